@@ -1,0 +1,37 @@
+# Build of the B200 evaluator (libvp_b200.so) and the CPU oracle.
+#   make          -> paper_2205_04401_b200/libvp_b200.so + oracle/liboracle.so
+#   make ref      -> oracle/_ref/libvpref.so (needs /root/reference; test pinning only)
+NVCC ?= nvcc
+CXX := /usr/bin/g++
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_2205_04401_b200
+CSRC := $(PKG)/csrc
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -v \
+           -Xcompiler -fPIC,-ffp-contract=off -Iinclude -I$(CSRC) -ccbin $(CXX)
+CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(CSRC)
+
+LIB := $(PKG)/libvp_b200.so
+OBJS := $(CSRC)/vp_b200.o $(CSRC)/vp_setup.o
+
+all: $(LIB) oracle
+
+$(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/koorn.cuh include/vp.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; exit 1)
+
+$(CSRC)/vp_setup.o: $(CSRC)/vp_setup.cpp $(CSRC)/koorn.cuh include/vp_setup.h
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(OBJS) -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -f $(OBJS) $(LIB) $(CSRC)/ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle ref clean

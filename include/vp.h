@@ -1,0 +1,135 @@
+/* vp.h -- C-ABI of the B200 volume-potential evaluator (libvp_b200.so).
+ *
+ * Drop-in for the hot path of the reference's evaluate_field
+ * (SPEC.md:582-590): mesh + per-triangle order-p Koornwinder density in,
+ * potentials u(x) = (1/2pi) int log|x-y| f(y) dy at targets out.  The
+ * reference has no FFI layer of its own; each entry point
+ * cites the reference (SPEC) operation it replaces.  INTEGRATION.md shows
+ * the binding a reference maintainer would add.
+ *
+ * Conventions (mirroring the reference):
+ *   - plain pointers and sizes, caller owns every host array;
+ *   - a context is bound to one CUDA device (one process per GPU) and is
+ *     immutable between vp_set_* calls; vp_evaluate on one context is
+ *     serialised on its stream, distinct contexts may run concurrently
+ *     (SPEC.md:543, :623-624);
+ *   - return 0 ok, 1 usage / invalid argument, 2 numerical failure,
+ *     3 device error (SPEC.md:730 exit codes + a device code); the message
+ *     names the violated invariant (rules.hpp:58-85) via vp_last_error.
+ *   - there is no CPU fallback: without a usable sm_100 device every
+ *     compute entry point returns 3.
+ */
+#ifndef VP_H
+#define VP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vp_ctx vp_ctx;
+
+/* Rules on the reference simplex Delta^1 = {x,y >= 0, x+y <= 1}.
+ * Replaces load_far_rule / load_rule (rules.hpp:88-125), the near rule of
+ * near_eval (N_n) and the SelfRule:
+ * radial GGQ (ggq.hpp:17-22) and Gauss-Legendre (gauss.hpp:17-46). */
+typedef struct {
+  int q;          /* far rule polynomial order N (sizes the near field) */
+  int len_q;
+  const double* far_x;
+  const double* far_y;
+  const double* far_w;
+  int n_n;        /* near rule order N_n (12) */
+  int len_n;
+  const double* near_x;
+  const double* near_y;
+  const double* near_w;
+  int n_l;        /* Gauss-Legendre length N_l (16), nodes on [-1,1] */
+  const double* gl_x;
+  const double* gl_w;
+  int n_g;        /* GGQ order N_g (8): n_g+1 nodes on (0,1) */
+  const double* ggq_r;
+  const double* ggq_w;
+  double eps;     /* tolerance epsilon of the near-field model (for:rho0) */
+} vp_rules;
+
+typedef struct {
+  int64_t n_targets;
+  int64_t n_outside;    /* targets with S(t) = -1 (exclusion list) */
+  int64_t n_near_pairs; /* sum |N(t)| */
+  int64_t n_self;       /* targets with a self pair */
+  int64_t n_leaves;     /* accepted near sub-simplices; s_n = n_leaves / n_targets */
+  int64_t n_panels;     /* arc-length panels; s_l = n_panels / n_self */
+  int64_t n_rho_le1;    /* sub-simplices accepted with rho_d <= 1 */
+  int64_t n_degenerate; /* self sub-triangles skipped (target on a side line) */
+  int64_t n_sources;    /* far-field point sources (n_tri * len_q) */
+  int32_t max_depth;
+  int32_t gpu_launches; /* kernels launched by this call */
+  double t_list_ms;     /* device time: near-field list build (K3) */
+  double t_far_ms;      /* device time: strengths + far sum (K1, K2): T_F */
+  double t_near_ms;     /* device time: near pairs (K4): T_N */
+  double t_self_ms;     /* device time: self pairs (K5): T_S */
+  double t_total_ms;    /* device time of the whole evaluation */
+} vp_stats;
+
+/* context (device = CUDA ordinal) */
+int vp_create(int device, vp_ctx** out);
+void vp_destroy(vp_ctx* ctx);
+const char* vp_last_error(const vp_ctx* ctx);
+
+/* TriMesh restricted to straight triangles: vertices
+ * [n_vert*2], triangles [n_tri*3] counter-clockwise.  Affine element map
+ * rho_T(xi,eta) = v0 + xi (v1-v0) + eta (v2-v0). */
+int vp_set_mesh(vp_ctx* ctx, int64_t n_vert, const double* vxy, int64_t n_tri,
+                const int32_t* tri);
+
+/* Rules + tolerance; builds the per-element near-field models
+ * (build_model) on the host so list predicates are
+ * bit-reproducible, and the element bins used by the list build. */
+int vp_set_rules(vp_ctx* ctx, const vp_rules* rules);
+
+/* Density as order-p Koornwinder coefficients per triangle, [n_tri * M_p],
+ * graded order (koornwinder.hpp:12-21); p <= 12. */
+int vp_set_density(vp_ctx* ctx, int p, const double* coeffs);
+
+/* Near-field lists (locate + nearby + in_near_field, SPEC.md:368-386,
+ * :450-458): self_out[t] = S(t) (-1 outside), CSR offsets [n_tgt+1] and
+ * ascending element ids.  With ids_out == NULL only *n_ids is returned. */
+int vp_build_nearlist(vp_ctx* ctx, int64_t n_tgt, const double* txy, int32_t* self_out,
+                      int64_t* offsets_out, int32_t* ids_out, int64_t ids_cap,
+                      int64_t* n_ids);
+
+/* Full evaluation (evaluate_field phases 1-2 with the direct far path,
+ * SPEC.md:582-590, :618): u[t] = far sum + sum_{N(t)} (near_eval - point
+ * sum) + (self_eval - point sum).  Host arrays in and out. */
+int vp_evaluate(vp_ctx* ctx, int64_t n_tgt, const double* txy, double* u_out, vp_stats* st);
+
+/* Same with device-resident targets and output (pointers on ctx's device),
+ * for callers that keep data in HBM; `stream` may be NULL (ctx stream). */
+int vp_evaluate_device(vp_ctx* ctx, int64_t n_tgt, const double* d_txy, double* d_u,
+                       void* stream, vp_stats* st);
+
+/* Far field only (fmm_eval --direct): u_far[t] =
+ * sum_j q_j log r_tj^2, q_j = w_j |J| f_j / (4 pi); coincident pairs give 0. */
+int vp_far_field(vp_ctx* ctx, int64_t n_tgt, const double* txy, double* u_far);
+
+/* Point sources of the far field (ChargeSystem):
+ * sx, sy, q [n_tri * len_q], element-major. */
+int vp_sources(vp_ctx* ctx, double* sx, double* sy, double* q);
+
+/* Per-pair corrections for explicit (target, element) pairs: near_eval
+ * and the point sum it replaces; and self_eval
+ * for targets inside `elem`.  leaves/panels per pair. */
+int vp_near_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t* elem,
+                  double* val, double* sub, int64_t* leaves);
+int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t* elem,
+                  double* val, double* sub, int64_t* panels);
+
+/* Roofline bookkeeping for the bench: device time of the last far-field
+ * kernel launch sequence and its launch count. */
+int vp_device_info(vp_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,91 @@
+/* vp_setup.h -- host-side setup for the volume-potential evaluator.
+ *
+ * Everything here runs once per problem on the host (C++), producing the
+ * inputs the evaluator's C-ABI (vp.h) consumes: quadrature rules on the
+ * reference simplex, the 1-D rules of self-interaction, synthetic meshes,
+ * target sets and per-triangle Koornwinder density coefficients.
+ *
+ * Reference anchors:
+ *   - rules are data in the reference (rules.hpp:88-125); its
+ *     Xiao-Gimbutas / Vioreanu-Rokhlin tables are absent, so
+ *     vps_simplex_rule builds a collapsed Gauss-Jacobi substitute that passes
+ *     the reference's validate_rule contract (rules.hpp:60-85);
+ *   - vps_gauss_legendre restates gauss_legendre (gauss.hpp:17-46);
+ *   - vps_ggq restates build_ggq's moment fitting (ggq.hpp:33-182);
+ *   - density coefficients replace the reference's callable f
+ *     with per-triangle order-p Koornwinder coefficients (BASELINE.json north_star).
+ * Return codes: 0 ok, 1 usage error, 2 numerical failure.
+ */
+#ifndef VP_SETUP_H
+#define VP_SETUP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* number of Koornwinder modes (p+1)(p+2)/2 (koornwinder.hpp:20) */
+int vps_koorn_size(int p);
+
+/* Gauss-Legendre on [-1,1] (gauss.hpp:17-46) */
+int vps_gauss_legendre(int n, double* x, double* w);
+
+/* Gauss-Jacobi for the weight (1-u) on [0,1], n nodes */
+int vps_gauss_jacobi10(int n, double* x, double* w);
+
+/* Simplex rule exact to total degree `order`: collapsed Gauss-Jacobi with
+ * n = floor(order/2)+1 points per direction, len = n*n.  Query the length
+ * with x == NULL. */
+int vps_simplex_rule(int order, int* len, double* x, double* y, double* w);
+
+/* Radial generalized Gaussian rule: ng+1 nodes on (0,1) integrating
+ * r P_n(2r-1) and r log r P_n(2r-1), n <= ng (ggq.hpp:13-22, :96-182). */
+int vps_ggq(int ng, double* r, double* w, double* max_residual);
+
+/* Target nodes on the reference simplex: shifted principal lattice
+ * ((i+1)/(p+3), (j+1)/(p+3)), i+j <= p; (p+1)(p+2)/2 nodes. */
+int vps_lattice_nodes(int p, double* x, double* y);
+
+/* analytic densities used by the synthetic configurations */
+enum {
+  VPS_F_CONST = 0,     /* params[0] */
+  VPS_F_SQUARE = 1,    /* sin(3x)cos(2y) + x^2 */
+  VPS_F_GAUSS = 2,     /* exp(-params[2] |x-(params[0],params[1])|^2) */
+  VPS_F_BUMPS = 3,     /* sum_k A_k exp(-|x-c_k|^2/s_k^2), params = n_bumps x (cx,cy,s,A) */
+  VPS_F_COSSIN = 4,    /* cos(4 pi x) sin(2 pi y) */
+  VPS_F_LINEAR = 5     /* params[0] + params[1] x + params[2] y */
+};
+double vps_density_eval(int kind, const double* params, int n_params, double x, double y);
+
+/* L2 projection of an analytic density onto the order-p Koornwinder basis
+ * of every triangle: c_T,j = int_{Delta^1} f(rho_T(xi)) K_j(xi) dxi. */
+int vps_project_density(int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri,
+                        int p, int kind, const double* params, int n_params, double* coeffs);
+
+/* Synthetic configurations of BASELINE.json:configs (1-based id 1..5).
+ * q_override > 0 replaces the config's far order (config 5 sweep). */
+typedef struct {
+  int64_t n_vert;
+  int64_t n_tri;
+  int64_t n_tgt;
+  int p;
+  int q;
+  int density_kind;
+  int n_params;
+  double params[64];
+  double eps;
+  uint64_t seed;
+  int staggered; /* targets on a separate staggered mesh */
+  int pad;
+} vps_config_info;
+
+int vps_config_info_get(int config, int q_override, uint64_t seed, vps_config_info* info);
+int vps_config_fill(int config, int q_override, uint64_t seed, double* vxy, int32_t* tri,
+                    double* txy, double* coeffs);
+
+const char* vps_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,221 @@
+"""ctypes binding of the CPU oracle (liboracle.so) and the reference shim
+(oracle/_ref/libvpref.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py, as the checker.  The
+product package (paper_2205_04401_b200) never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libvpref.so")
+
+_d_p = ctypes.POINTER(ctypes.c_double)
+_i32_p = ctypes.POINTER(ctypes.c_int32)
+_i64_p = ctypes.POINTER(ctypes.c_int64)
+
+
+def _d(a):
+    return a.ctypes.data_as(_d_p)
+
+
+class VpoProblem(ctypes.Structure):
+    _fields_ = [
+        ("n_vert", ctypes.c_int64), ("vxy", _d_p), ("n_tri", ctypes.c_int64), ("tri", _i32_p),
+        ("p", ctypes.c_int), ("coeffs", _d_p),
+        ("q", ctypes.c_int), ("len_q", ctypes.c_int), ("far_x", _d_p), ("far_y", _d_p), ("far_w", _d_p),
+        ("n_n", ctypes.c_int), ("len_n", ctypes.c_int), ("near_x", _d_p), ("near_y", _d_p),
+        ("near_w", _d_p),
+        ("n_l", ctypes.c_int), ("gl_x", _d_p), ("gl_w", _d_p),
+        ("n_g", ctypes.c_int), ("ggq_r", _d_p), ("ggq_w", _d_p),
+        ("eps", ctypes.c_double),
+    ]
+
+
+class VpoStats(ctypes.Structure):
+    _fields_ = [
+        ("n_targets", ctypes.c_int64), ("n_outside", ctypes.c_int64), ("n_near_pairs", ctypes.c_int64),
+        ("n_self", ctypes.c_int64), ("n_leaves", ctypes.c_int64), ("n_panels", ctypes.c_int64),
+        ("n_rho_le1", ctypes.c_int64), ("n_degenerate", ctypes.c_int64),
+        ("max_depth", ctypes.c_int32), ("pad", ctypes.c_int32),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(ORACLE_PATH)
+        L.vpo_last_error.restype = ctypes.c_char_p
+        L.vpo_cn_lookup.restype = ctypes.c_double
+        L.vpo_w_edge.restype = ctypes.c_double
+        _lib = L
+    return _lib
+
+
+def ref():
+    """The reference's own headers behind an extern "C" shim (None if not built)."""
+    global _ref
+    if _ref is None and os.path.exists(REF_PATH):
+        _ref = ctypes.CDLL(REF_PATH)
+    return _ref
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().vpo_last_error().decode())
+
+
+class Oracle:
+    """Holds the arrays of one problem and exposes the oracle entry points."""
+
+    def __init__(self, vxy, tri, p, coeffs, rules):
+        self.vxy = np.ascontiguousarray(vxy, dtype=np.float64).reshape(-1, 2)
+        self.tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
+        self.coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        self.p = p
+        self.rules = rules
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64)
+                      for a in (*rules.far, *rules.near, *rules.gl, *rules.ggq)]
+        k = self._keep
+        self.pr = VpoProblem(
+            n_vert=self.vxy.shape[0], vxy=_d(self.vxy), n_tri=self.tri.shape[0],
+            tri=self.tri.ctypes.data_as(_i32_p), p=p, coeffs=_d(self.coeffs),
+            q=rules.q, len_q=len(k[0]), far_x=_d(k[0]), far_y=_d(k[1]), far_w=_d(k[2]),
+            n_n=rules.n_n, len_n=len(k[3]), near_x=_d(k[3]), near_y=_d(k[4]), near_w=_d(k[5]),
+            n_l=len(k[6]), gl_x=_d(k[6]), gl_w=_d(k[7]),
+            n_g=rules.n_g, ggq_r=_d(k[8]), ggq_w=_d(k[9]), eps=rules.eps)
+
+    @classmethod
+    def from_problem(cls, pr):
+        return cls(pr.vxy, pr.tri, pr.p, pr.coeffs, pr.rules)
+
+    def nearlist(self, txy):
+        t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)
+        n = t.shape[0]
+        nids = ctypes.c_int64()
+        L = lib()
+        _check(L.vpo_nearlist(ctypes.byref(self.pr), n, _d(t), None, None, None, 0, ctypes.byref(nids)))
+        s = np.zeros(n, dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.int64)
+        ids = np.zeros(max(nids.value, 1), dtype=np.int32)
+        _check(L.vpo_nearlist(ctypes.byref(self.pr), n, _d(t), s.ctypes.data_as(_i32_p),
+                              off.ctypes.data_as(_i64_p), ids.ctypes.data_as(_i32_p), ids.size,
+                              ctypes.byref(nids)))
+        return s, off, ids[:nids.value]
+
+    def sources(self):
+        n = self.tri.shape[0] * len(self.rules.far[0])
+        sx, sy, q = np.zeros(n), np.zeros(n), np.zeros(n)
+        _check(lib().vpo_sources(ctypes.byref(self.pr), _d(sx), _d(sy), _d(q)))
+        return sx, sy, q
+
+    def far_sum(self, txy, nthreads=0):
+        t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)
+        u = np.zeros(t.shape[0])
+        _check(lib().vpo_far_sum(ctypes.byref(self.pr), t.shape[0], _d(t), nthreads, _d(u)))
+        return u
+
+    def near_pair(self, tx, ty, elem):
+        v, s, lv, dp = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().vpo_near_pair(ctypes.byref(self.pr), ctypes.c_double(tx), ctypes.c_double(ty),
+                                   int(elem), ctypes.byref(v), ctypes.byref(s), ctypes.byref(lv),
+                                   ctypes.byref(dp)))
+        return v.value, s.value, lv.value, dp.value
+
+    def self_pair(self, tx, ty, elem):
+        v, s, pn = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(lib().vpo_self(ctypes.byref(self.pr), ctypes.c_double(tx), ctypes.c_double(ty), int(elem),
+                              ctypes.byref(v), ctypes.byref(s), ctypes.byref(pn)))
+        return v.value, s.value, pn.value
+
+    def evaluate(self, txy, nthreads=0):
+        t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)
+        u, uf = np.zeros(t.shape[0]), np.zeros(t.shape[0])
+        st = VpoStats()
+        _check(lib().vpo_evaluate(ctypes.byref(self.pr), t.shape[0], _d(t), nthreads, _d(u), _d(uf),
+                                  ctypes.byref(st)))
+        return u, uf, st.as_dict()
+
+    def element_models(self):
+        E = self.tri.shape[0]
+        rho0, rho0n, ta = np.zeros(E), np.zeros(E), np.zeros(3 * E)
+        _check(lib().vpo_element_models(ctypes.byref(self.pr), _d(rho0), _d(rho0n), _d(ta)))
+        return rho0, rho0n, ta.reshape(E, 3)
+
+
+def koornwinder(order, x, y):
+    out = np.zeros((order + 1) * (order + 2) // 2)
+    _check(lib().vpo_koornwinder(order, ctypes.c_double(x), ctypes.c_double(y), _d(out)))
+    return out
+
+
+def cn_lookup(n):
+    return lib().vpo_cn_lookup(n)
+
+
+def w_edge(x, y, w):
+    x, y, w = (np.ascontiguousarray(a, dtype=np.float64) for a in (x, y, w))
+    return lib().vpo_w_edge(len(x), _d(x), _d(y), _d(w))
+
+
+def validate_rule(order, x, y, w):
+    x, y, w = (np.ascontiguousarray(a, dtype=np.float64) for a in (x, y, w))
+    _check(lib().vpo_validate_rule(order, len(x), _d(x), _d(y), _d(w)))
+
+
+def gauss_legendre(n):
+    x, w = np.zeros(n), np.zeros(n)
+    _check(lib().vpo_gauss_legendre(n, _d(x), _d(w)))
+    return x, w
+
+
+def quadtree_query(pts, leaf_cap, rect, use_ref=False):
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+    n = ctypes.c_int64()
+    vis = ctypes.c_int64()
+    L = ref() if use_ref else lib()
+    fn = L.vpref_quadtree_query if use_ref else L.vpo_quadtree_query
+    args = [pts.shape[0], _d(pts), leaf_cap] + [ctypes.c_double(v) for v in rect]
+    rc = fn(*args, None, 0, ctypes.byref(n), ctypes.byref(vis))
+    if rc:
+        raise OracleError(rc, "quadtree query failed")
+    out = np.zeros(max(n.value, 1), dtype=np.int32)
+    rc = fn(*args, out.ctypes.data_as(_i32_p), out.size, ctypes.byref(n), ctypes.byref(vis))
+    if rc:
+        raise OracleError(rc, "quadtree query failed")
+    return out[:n.value], vis.value
+
+
+def ref_koornwinder(order, x, y):
+    out = np.zeros((order + 1) * (order + 2) // 2)
+    rc = ref().vpref_koornwinder(order, ctypes.c_double(x), ctypes.c_double(y), _d(out))
+    if rc:
+        raise OracleError(rc, "reference koornwinder_eval: point outside the reference simplex")
+    return out
+
+
+def ref_gauss_legendre(n):
+    x, w = np.zeros(n), np.zeros(n)
+    rc = ref().vpref_gauss_legendre(n, _d(x), _d(w))
+    if rc:
+        raise OracleError(rc, "reference gauss_legendre failed")
+    return x, w

@@ -1,0 +1,380 @@
+"""Host-side mirror of the reference's evaluation interface for the hot path.
+
+Names follow the reference specification so a user of the reference finds
+the same entry points (SPEC.md module -> here):
+
+  basis      koornwinder size, rules        simplex_rule, gauss_legendre, build_ggq
+  nearfield  cn_lookup                      cn_lookup
+  element-map / nearfield                   Evaluator.build_nearlist (locate+nearby+in_near_field)
+  quadrature-engine                         near_eval / self_eval / far_eval (per pair, GPU)
+  fmm-pipeline                              fmm_eval(direct=True), evaluate_field
+
+Every compute call goes through the C-ABI of libvp_b200.so (include/vp.h);
+errors map to the reference's exception kinds: UsageError
+(std::invalid_argument, code 1), NumericalError (std::runtime_error /
+std::domain_error, code 2), DeviceError (code 3, no usable B200).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import VpRules, VpStats, VpsConfigInfo, c_double_p, c_int32_p, c_int64_p
+
+
+class VolpotError(RuntimeError):
+    code = 0
+
+
+class UsageError(VolpotError, ValueError):
+    code = 1
+
+
+class NumericalError(VolpotError):
+    code = 2
+
+
+class DeviceError(VolpotError):
+    code = 3
+
+
+_ERRS = {1: UsageError, 2: NumericalError, 3: DeviceError}
+
+
+def _check(rc: int, msg: str):
+    if rc != 0:
+        raise _ERRS.get(rc, VolpotError)(f"[{rc}] {msg}")
+
+
+def _d(a):
+    return a.ctypes.data_as(c_double_p)
+
+
+def _i32(a):
+    return a.ctypes.data_as(c_int32_p)
+
+
+def _i64(a):
+    return a.ctypes.data_as(c_int64_p)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def _setup_err():
+    return _lib.lib().vps_last_error().decode()
+
+
+# ---------------------------------------------------------------------------
+# basis / rules (host setup)
+
+def koorn_size(p: int) -> int:
+    """(p+1)(p+2)/2 (koornwinder.hpp:20)."""
+    return (p + 1) * (p + 2) // 2
+
+
+def koorn_index(m: int, n: int) -> int:
+    """graded index n(n+1)/2 + m (koornwinder.hpp:21)."""
+    return n * (n + 1) // 2 + m
+
+
+def cn_lookup(n: int) -> float:
+    """C_N calibration.  Orders below
+    12 are clamped to C_12 = 12 (policy SURVEY.md §9.3; the reference errors)."""
+    kn = [12, 20, 25, 30, 40, 50]
+    kc = [12.0, 6.8, 3.0, 2.5, 2.0, 1.0]
+    if n <= 12:
+        return 12.0
+    if n >= 50:
+        return 1.0
+    for i in range(5):
+        if n == kn[i]:
+            return kc[i]
+        if kn[i] < n < kn[i + 1]:
+            f = float(n - kn[i]) / float(kn[i + 1] - kn[i])
+            return kc[i] + (kc[i + 1] - kc[i]) * f
+    return 1.0
+
+
+def simplex_rule(order: int):
+    """(x, y, w) of the order-`order` collapsed Gauss-Jacobi rule on Delta^1."""
+    L = _lib.lib()
+    n = ctypes.c_int()
+    _check(L.vps_simplex_rule(order, ctypes.byref(n), None, None, None), _setup_err())
+    x, y, w = (np.zeros(n.value) for _ in range(3))
+    _check(L.vps_simplex_rule(order, ctypes.byref(n), _d(x), _d(y), _d(w)), _setup_err())
+    return x, y, w
+
+
+def gauss_legendre(n: int):
+    """Gauss-Legendre on [-1, 1] (gauss.hpp:17-46)."""
+    x, w = np.zeros(n), np.zeros(n)
+    _check(_lib.lib().vps_gauss_legendre(n, _d(x), _d(w)), _setup_err())
+    return x, w
+
+
+def build_ggq(ng: int):
+    """Radial GGQ rule with ng+1 nodes (ggq.hpp:96-182); returns (r, w, residual)."""
+    r, w, res = np.zeros(ng + 1), np.zeros(ng + 1), ctypes.c_double()
+    _check(_lib.lib().vps_ggq(ng, _d(r), _d(w), ctypes.byref(res)), _setup_err())
+    return r, w, res.value
+
+
+def lattice_nodes(p: int):
+    m = koorn_size(p)
+    x, y = np.zeros(m), np.zeros(m)
+    _check(_lib.lib().vps_lattice_nodes(p, _d(x), _d(y)), _setup_err())
+    return x, y
+
+
+@dataclass
+class Rules:
+    """Everything vp_set_rules needs (far rule of order q, near rule N_n,
+    GL N_l, GGQ N_g, tolerance eps).  Defaults mirror SPEC.md:733."""
+    q: int
+    far: tuple
+    n_n: int
+    near: tuple
+    gl: tuple
+    n_g: int
+    ggq: tuple
+    eps: float
+
+    def as_struct(self) -> VpRules:
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64)
+                      for a in (*self.far, *self.near, *self.gl, *self.ggq)]
+        k = self._keep
+        return VpRules(q=self.q, len_q=len(k[0]), far_x=_d(k[0]), far_y=_d(k[1]), far_w=_d(k[2]),
+                       n_n=self.n_n, len_n=len(k[3]), near_x=_d(k[3]), near_y=_d(k[4]),
+                       near_w=_d(k[5]), n_l=len(k[6]), gl_x=_d(k[6]), gl_w=_d(k[7]),
+                       n_g=self.n_g, ggq_r=_d(k[8]), ggq_w=_d(k[9]), eps=self.eps)
+
+
+def make_rules(q: int, n_n: int = 12, n_l: int = 16, n_g: int = 8, eps: float = 1e-12) -> Rules:
+    r, w, _ = build_ggq(n_g)
+    return Rules(q=q, far=simplex_rule(q), n_n=n_n, near=simplex_rule(n_n), gl=gauss_legendre(n_l),
+                 n_g=n_g, ggq=(r, w), eps=eps)
+
+
+def project_density(vxy, tri, p: int, kind: int, params=()):
+    """Per-triangle Koornwinder coefficients of an analytic density (L2 projection)."""
+    vxy = _f64(vxy, (-1, 2))
+    tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
+    prm = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(-1))
+    if prm.size == 0:
+        prm = np.zeros(1)
+    out = np.zeros((tri.shape[0], koorn_size(p)))
+    _check(_lib.lib().vps_project_density(vxy.shape[0], _d(vxy), tri.shape[0], _i32(tri), p, kind,
+                                          _d(prm), len(params), _d(out)), _setup_err())
+    return out
+
+
+def density_eval(kind: int, params, x: float, y: float) -> float:
+    prm = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(-1))
+    if prm.size == 0:
+        prm = np.zeros(1)
+    return _lib.lib().vps_density_eval(kind, _d(prm), len(params), x, y)
+
+
+F_CONST, F_SQUARE, F_GAUSS, F_BUMPS, F_COSSIN, F_LINEAR = range(6)
+
+
+@dataclass
+class Problem:
+    """A mesh, density coefficients, targets and rules (one BASELINE config)."""
+    config: int
+    vxy: np.ndarray
+    tri: np.ndarray
+    txy: np.ndarray
+    coeffs: np.ndarray
+    p: int
+    q: int
+    eps: float
+    seed: int
+    density_kind: int
+    params: np.ndarray
+    staggered: bool
+    rules: Rules = field(default=None)
+
+    @property
+    def n_tri(self):
+        return self.tri.shape[0]
+
+    @property
+    def n_tgt(self):
+        return self.txy.shape[0]
+
+
+def config_info(cfg: int, q_override: int = 0, seed: int = 0) -> dict:
+    info = VpsConfigInfo()
+    _check(_lib.lib().vps_config_info_get(cfg, q_override, seed, ctypes.byref(info)), _setup_err())
+    return {"n_vert": info.n_vert, "n_tri": info.n_tri, "n_tgt": info.n_tgt, "p": info.p,
+            "q": info.q, "eps": info.eps, "density_kind": info.density_kind,
+            "params": np.array(info.params[:info.n_params]), "staggered": bool(info.staggered)}
+
+
+def load_config(cfg: int, q_override: int = 0, seed: int = 0, with_rules: bool = True) -> Problem:
+    """Synthetic BASELINE.json config `cfg` (1..5) from the seeded generators."""
+    I = config_info(cfg, q_override, seed)
+    vxy = np.zeros((I["n_vert"], 2))
+    tri = np.zeros((I["n_tri"], 3), dtype=np.int32)
+    txy = np.zeros((I["n_tgt"], 2))
+    coeffs = np.zeros((I["n_tri"], koorn_size(I["p"])))
+    _check(_lib.lib().vps_config_fill(cfg, q_override, seed, _d(vxy), _i32(tri), _d(txy), _d(coeffs)),
+           _setup_err())
+    pr = Problem(config=cfg, vxy=vxy, tri=tri, txy=txy, coeffs=coeffs, p=I["p"], q=I["q"], eps=I["eps"],
+                 seed=seed, density_kind=I["density_kind"], params=I["params"],
+                 staggered=I["staggered"])
+    if with_rules:
+        pr.rules = make_rules(pr.q, eps=pr.eps)
+    return pr
+
+
+# ---------------------------------------------------------------------------
+# evaluator (GPU, through the C-ABI)
+
+class Evaluator:
+    """One context on one CUDA device (one process per GPU)."""
+
+    def __init__(self, device: int = 0):
+        self._L = _lib.lib()
+        h = ctypes.c_void_p()
+        rc = self._L.vp_create(device, ctypes.byref(h))
+        if rc != 0:
+            raise _ERRS.get(rc, VolpotError)(
+                f"[{rc}] vp_create(device={device}) failed: no usable sm_100 device "
+                "(there is no CPU fallback)")
+        self._h = h
+        self.device = device
+        self.p = None
+        self.n_tri = 0
+
+    def _err(self):
+        return self._L.vp_last_error(self._h).decode()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.vp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_mesh(self, vxy, tri):
+        self._vxy = _f64(vxy, (-1, 2))
+        self._tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
+        _check(self._L.vp_set_mesh(self._h, self._vxy.shape[0], _d(self._vxy), self._tri.shape[0],
+                                   _i32(self._tri)), self._err())
+        self.n_tri = self._tri.shape[0]
+
+    def set_rules(self, rules: Rules):
+        self._rules_struct = rules.as_struct()
+        self._rules = rules
+        _check(self._L.vp_set_rules(self._h, ctypes.byref(self._rules_struct)), self._err())
+
+    def set_density(self, p: int, coeffs):
+        c = _f64(coeffs)
+        _check(self._L.vp_set_density(self._h, p, _d(c)), self._err())
+        self.p = p
+
+    def load(self, pr: Problem):
+        self.set_mesh(pr.vxy, pr.tri)
+        self.set_rules(pr.rules)
+        self.set_density(pr.p, pr.coeffs)
+        return self
+
+    def build_nearlist(self, txy):
+        """(S, offsets, ids): S(t) (-1 outside), CSR of N(t) ascending."""
+        t = _f64(txy, (-1, 2))
+        n = t.shape[0]
+        nids = ctypes.c_int64()
+        self_ = np.zeros(n, dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.int64)
+        _check(self._L.vp_build_nearlist(self._h, n, _d(t), _i32(self_), _i64(off), None, 0,
+                                         ctypes.byref(nids)), self._err())
+        ids = np.zeros(max(nids.value, 1), dtype=np.int32)
+        _check(self._L.vp_build_nearlist(self._h, n, _d(t), _i32(self_), _i64(off), _i32(ids),
+                                         ids.size, ctypes.byref(nids)), self._err())
+        return self_, off, ids[:nids.value]
+
+    def evaluate(self, txy):
+        """u at the targets and the run statistics (evaluate_field core)."""
+        t = _f64(txy, (-1, 2))
+        u = np.zeros(t.shape[0])
+        st = VpStats()
+        _check(self._L.vp_evaluate(self._h, t.shape[0], _d(t), _d(u), ctypes.byref(st)), self._err())
+        return u, st.as_dict()
+
+    def evaluate_device(self, n: int, d_txy: int, d_u: int, stream: int = 0):
+        st = VpStats()
+        _check(self._L.vp_evaluate_device(self._h, n, ctypes.c_void_p(d_txy), ctypes.c_void_p(d_u),
+                                          ctypes.c_void_p(stream or None), ctypes.byref(st)),
+               self._err())
+        return st.as_dict()
+
+    def far_field(self, txy):
+        t = _f64(txy, (-1, 2))
+        u = np.zeros(t.shape[0])
+        _check(self._L.vp_far_field(self._h, t.shape[0], _d(t), _d(u)), self._err())
+        return u
+
+    def sources(self):
+        n = self.n_tri * len(self._rules.far[0])
+        sx, sy, q = np.zeros(n), np.zeros(n), np.zeros(n)
+        _check(self._L.vp_sources(self._h, _d(sx), _d(sy), _d(q)), self._err())
+        return sx, sy, q
+
+    def _pairs(self, fn, txy, elem):
+        t = _f64(txy, (-1, 2))
+        e = np.ascontiguousarray(elem, dtype=np.int32).reshape(-1)
+        n = t.shape[0]
+        val, sub, cnt = np.zeros(n), np.zeros(n), np.zeros(n, dtype=np.int64)
+        _check(fn(self._h, n, _d(t), _i32(e), _d(val), _d(sub), _i64(cnt)), self._err())
+        return val, sub, cnt
+
+    def near_pairs(self, txy, elem):
+        """near_eval(T, t), the point sum it replaces, and leaf counts."""
+        return self._pairs(self._L.vp_near_pairs, txy, elem)
+
+    def self_pairs(self, txy, elem):
+        """self_eval(T, t), the point sum it replaces, and panel counts."""
+        return self._pairs(self._L.vp_self_pairs, txy, elem)
+
+
+def evaluate_field(pr: Problem, targets=None, device: int = 0):
+    """evaluate_field, direct far path: potentials at the
+    targets plus statistics c, s_n, s_l and the device-time split."""
+    with Evaluator(device) as ev:
+        ev.load(pr)
+        u, st = ev.evaluate(pr.txy if targets is None else targets)
+    n = max(st["n_targets"], 1)
+    st["c"] = (st["n_near_pairs"] + st["n_self"]) / n
+    st["s_n"] = st["n_leaves"] / n
+    st["s_l"] = st["n_panels"] / max(st["n_self"], 1)
+    return u, st
+
+
+def fmm_eval(pr: Problem, targets=None, direct: bool = True, device: int = 0):
+    """fmm_eval -- only the direct O(N^2) path is on the hot
+    path; the FMM itself is the next row."""
+    if not direct:
+        raise UsageError("[1] fmm_eval: only the direct path is implemented (SURVEY.md §8(f1))")
+    with Evaluator(device) as ev:
+        ev.load(pr)
+        return ev.far_field(pr.txy if targets is None else targets)

@@ -1,0 +1,1380 @@
+// vp_b200.cu -- B200 (sm_100a) evaluator for the 2-D log-kernel volume
+// potential: kernels K1-K5 and the C-ABI of include/vp.h.
+//
+//   K1 k_sources   ChargeSystem strengths       FP64, tiny
+//   K2 k_far       direct far sum          FP64 pipe
+//   K3 k_lists     S(t), N(t) CSR      HBM/latency
+//   K4 k_near      near_eval - point sum         FP64 pipe
+//   K5 k_self      self_eval - point sum         FP64 pipe
+//   k_assemble     subtract-and-add
+//
+// Data stays resident in HBM inside the context; every per-target result is
+// produced by a fixed-order reduction, so u is deterministic run to run and
+// independent of how targets are sharded across GPUs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "vp.h"
+#include "vp_device.cuh"
+
+using namespace vp;
+
+namespace {
+
+constexpr int kMaxPdev = 12;
+constexpr int kMaxModes = (kMaxPdev + 1) * (kMaxPdev + 2) / 2;  // 91
+constexpr int kMaxFar = 512;
+constexpr int kMaxNearRule = 256;
+constexpr int kMaxGL = 64;
+constexpr int kMaxGGQ = 32;
+
+__constant__ double c_cn[kMaxModes];  // Koornwinder normalisation c_mn by index
+
+struct RulesDev {
+  int len_q, len_n, n_l, n_g1, n_n, q;
+  double far_x[kMaxFar], far_y[kMaxFar], far_w[kMaxFar];
+  double near_x[kMaxNearRule], near_y[kMaxNearRule], near_w[kMaxNearRule];
+  double gl_x[kMaxGL], gl_w[kMaxGL];
+  double ggq_r[kMaxGGQ], ggq_w[kMaxGGQ], ggq_lr[kMaxGGQ];
+  double kd[kMaxNearDepth + 2];  // 4^{-d/N_n}
+};
+
+struct GridDev {
+  double x0, y0, cs, inv_cs;
+  int nx, ny;
+};
+
+// ---------------------------------------------------------------------------
+// K1: point sources y_i = rho_T(xi_i), q_i = w_i |J_T| f_T(xi_i) / (4 pi).
+// f_T(xi_i) = V[i,:] . c_T with V the Koornwinder values at the far nodes.
+__global__ void k_sources(int64_t E, int len_q, int M, const ElemRec* __restrict__ el,
+                          const double* __restrict__ coeffs, const double* __restrict__ V,
+                          const RulesDev* __restrict__ R, double* __restrict__ sx,
+                          double* __restrict__ sy, double* __restrict__ sq) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= E * len_q) return;
+  const int64_t e = s / len_q;
+  const int i = (int)(s - e * len_q);
+  const ElemRec& T = el[e];
+  const double xi = R->far_x[i], eta = R->far_y[i];
+  sx[s] = T.x0 + (xi * T.e1x + eta * T.e2x);
+  sy[s] = T.y0 + (xi * T.e1y + eta * T.e2y);
+  const double* c = coeffs + e * M;
+  const double* v = V + (int64_t)i * M;
+  double f = 0.0;
+  for (int j = 0; j < M; ++j) f = fma(c[j], v[j], f);
+  sq[s] = (R->far_w[i] * T.det) * f * kInv4Pi;
+}
+
+// ---------------------------------------------------------------------------
+// element binning for the list build: every element is entered in each grid
+// cell its near-field bbox overlaps.
+__device__ __forceinline__ int cell_coord(double x, double x0, double inv_cs, int n) {
+  const double f = floor(rn_mul(rn_sub(x, x0), inv_cs));
+  int c = f < 0.0 ? 0 : (f >= (double)n ? n - 1 : (int)f);
+  return c;
+}
+
+__global__ void k_bin_count(int64_t E, const ElemRec* __restrict__ el, GridDev g,
+                            int64_t* __restrict__ cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const ElemRec& T = el[e];
+  if (T.ta0 < 0.0) {
+    cnt[e] = 0;
+    return;
+  }
+  const int cx0 = cell_coord(T.bx0, g.x0, g.inv_cs, g.nx), cx1 = cell_coord(T.bx1, g.x0, g.inv_cs, g.nx);
+  const int cy0 = cell_coord(T.by0, g.y0, g.inv_cs, g.ny), cy1 = cell_coord(T.by1, g.y0, g.inv_cs, g.ny);
+  cnt[e] = (int64_t)(cx1 - cx0 + 1) * (cy1 - cy0 + 1);
+}
+
+__global__ void k_bin_fill(int64_t E, const ElemRec* __restrict__ el, GridDev g,
+                           const int64_t* __restrict__ off, int32_t* __restrict__ keys,
+                           int32_t* __restrict__ vals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const ElemRec& T = el[e];
+  if (T.ta0 < 0.0) return;
+  const int cx0 = cell_coord(T.bx0, g.x0, g.inv_cs, g.nx), cx1 = cell_coord(T.bx1, g.x0, g.inv_cs, g.nx);
+  const int cy0 = cell_coord(T.by0, g.y0, g.inv_cs, g.ny), cy1 = cell_coord(T.by1, g.y0, g.inv_cs, g.ny);
+  int64_t o = off[e];
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      keys[o] = cy * g.nx + cx;
+      vals[o] = (int32_t)e;
+      ++o;
+    }
+}
+
+__global__ void k_cell_ranges(int64_t n, const int32_t* __restrict__ keys,
+                              int64_t* __restrict__ beg, int64_t* __restrict__ end) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t k = keys[i];
+  if (i == 0 || keys[i - 1] != k) beg[k] = i;
+  if (i == n - 1 || keys[i + 1] != k) end[k] = i + 1;
+}
+
+// ---------------------------------------------------------------------------
+// K3: S(t) (lowest containing id) and N(t) (ascending) for every target.
+// Candidates = the elements binned in t's cell merged with the all-near list.
+template <bool FILL>
+__global__ void k_lists(int64_t T, const double2* __restrict__ txy,
+                        const ElemRec* __restrict__ el, GridDev g,
+                        const int64_t* __restrict__ cbeg, const int64_t* __restrict__ cend,
+                        const int32_t* __restrict__ celems, const int32_t* __restrict__ allnear,
+                        int n_allnear, int32_t* __restrict__ self_out,
+                        int64_t* __restrict__ cnt_out, const int64_t* __restrict__ off,
+                        int32_t* __restrict__ ids, double2* __restrict__ self_ref) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const double2 p = txy[t];
+  const double tx = p.x, ty = p.y;
+  int64_t b = 0, e = 0;
+  const double fx = floor(rn_mul(rn_sub(tx, g.x0), g.inv_cs));
+  const double fy = floor(rn_mul(rn_sub(ty, g.y0), g.inv_cs));
+  if (fx >= 0.0 && fy >= 0.0 && fx < (double)g.nx && fy < (double)g.ny) {
+    const int c = (int)fy * g.nx + (int)fx;
+    b = cbeg[c];
+    e = cend[c];
+  }
+  int32_t self = -1;
+  double sxi = 0.0, seta = 0.0;
+  int64_t n = 0;
+  int64_t o = FILL ? off[t] : 0;
+  int ia = 0;
+  while (b < e || ia < n_allnear) {
+    int32_t id;
+    const int32_t cb = b < e ? celems[b] : INT32_MAX;
+    const int32_t ca = ia < n_allnear ? allnear[ia] : INT32_MAX;
+    if (cb <= ca) {
+      id = cb;
+      ++b;
+      if (ca == cb) ++ia;
+    } else {
+      id = ca;
+      ++ia;
+    }
+    const ElemRec& R = el[id];
+    if (R.ta0 >= 0.0 && !(tx >= R.bx0 && tx <= R.bx1 && ty >= R.by0 && ty <= R.by1)) continue;
+    if (self < 0) {
+      double xi, eta;
+      if (rn_locate(R, tx, ty, xi, eta)) {
+        self = id;
+        sxi = xi;
+        seta = eta;
+        continue;
+      }
+    }
+    if (rn_in_near(R, tx, ty)) {
+      if (FILL) ids[o++] = id;
+      ++n;
+    }
+  }
+  if (!FILL) {
+    cnt_out[t] = n;
+    self_out[t] = self;
+    if (self_ref) self_ref[t] = make_double2(sxi, seta);
+  }
+}
+
+__global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* __restrict__ pt) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  for (int64_t p = off[t]; p < off[t + 1]; ++p) pt[p] = (int32_t)t;
+}
+
+// ---------------------------------------------------------------------------
+// K2: u_far[t] = sum_j q_j log r_tj^2 (coincident pairs contribute 0).
+// Sources are staged through shared memory and broadcast to the block's
+// targets; each thread keeps FAR_R targets in registers.  The source range
+// is split over gridDim.y; partials are reduced in fixed order.
+constexpr int FAR_THREADS = 256;
+constexpr int FAR_R = 4;
+constexpr int FAR_TILE = 512;
+
+__global__ void __launch_bounds__(FAR_THREADS) k_far(int64_t T, const double2* __restrict__ txy,
+                                                     int64_t S, const double* __restrict__ sx,
+                                                     const double* __restrict__ sy,
+                                                     const double* __restrict__ sq, int64_t chunk,
+                                                     double* __restrict__ part) {
+  __shared__ double shx[FAR_TILE], shy[FAR_TILE], shq[FAR_TILE];
+  const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
+  double tx[FAR_R], ty[FAR_R], acc[FAR_R];
+#pragma unroll
+  for (int r = 0; r < FAR_R; ++r) {
+    const int64_t t = tb + (int64_t)r * FAR_THREADS;
+    const double2 p = t < T ? txy[t] : make_double2(0.0, 0.0);
+    tx[r] = p.x;
+    ty[r] = p.y;
+    acc[r] = 0.0;
+  }
+  const int64_t s0 = (int64_t)blockIdx.y * chunk;
+  const int64_t s1 = min(S, s0 + chunk);
+  for (int64_t base = s0; base < s1; base += FAR_TILE) {
+    const int n = (int)min((int64_t)FAR_TILE, s1 - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += FAR_THREADS) {
+      shx[j] = sx[base + j];
+      shy[j] = sy[base + j];
+      shq[j] = sq[base + j];
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      const double px = shx[j], py = shy[j], q = shq[j];
+#pragma unroll
+      for (int r = 0; r < FAR_R; ++r) {
+        const double dx = tx[r] - px, dy = ty[r] - py;
+        const double r2 = fma(dx, dx, dy * dy);
+        const double lg = r2 > 0.0 ? log(r2) : 0.0;
+        acc[r] = fma(q, lg, acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < FAR_R; ++r) {
+    const int64_t t = tb + (int64_t)r * FAR_THREADS;
+    if (t < T) part[(int64_t)blockIdx.y * T + t] = acc[r];
+  }
+}
+
+__global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ part,
+                             double* __restrict__ u) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  double s = 0.0;
+  for (int k = 0; k < nsplit; ++k) s += part[(int64_t)k * T + t];
+  u[t] = s;
+}
+
+// sum_{i in T} q_i log r^2 of element e's sources, warp-cooperative
+__device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q, double tx,
+                                                 double ty, const double* __restrict__ sx,
+                                                 const double* __restrict__ sy,
+                                                 const double* __restrict__ sq) {
+  double s = 0.0;
+  for (int i = lane; i < len_q; i += 32) {
+    const int64_t k = e * len_q + i;
+    const double dx = tx - sx[k], dy = ty - sy[k];
+    const double r2 = fma(dx, dx, dy * dy);
+    if (r2 > 0.0) s = fma(sq[k], log(r2), s);
+  }
+  return warp_sum(s);
+}
+
+// ---------------------------------------------------------------------------
+// K4: near_eval over a warp-cooperative level-synchronous subdivision.
+// Sub-simplices are coded by their 2-bit child path; accepted leaves are
+// buffered and integrated lane-parallel over (leaf, node).
+constexpr int NEAR_WARPS = 4;
+constexpr int FCAP = 128;
+constexpr int LCAP = 64;
+constexpr int kMaxPathDepth = 31;
+
+struct NearWarpSmem {
+  unsigned long long fpath[2][FCAP];
+  unsigned char fdep[2][FCAP];
+  double la[LCAP], lb[LCAP], lc[LCAP], ld[LCAP], le[LCAP], lf[LCAP], ls[LCAP];
+  double cc[kMaxModes];
+};
+
+__device__ __forceinline__ void decode_path(unsigned long long path, int d, double& ax, double& ay,
+                                            double& bx, double& by, double& cx, double& cy) {
+  ax = 0.0; ay = 0.0; bx = 1.0; by = 0.0; cx = 0.0; cy = 1.0;
+  for (int l = d - 1; l >= 0; --l) {
+    const int ch = (int)((path >> (2 * l)) & 3ull);
+    const double abx = (ax + bx) * 0.5, aby = (ay + by) * 0.5;
+    const double bcx = (bx + cx) * 0.5, bcy = (by + cy) * 0.5;
+    const double cax = (cx + ax) * 0.5, cay = (cy + ay) * 0.5;
+    if (ch == 0) { bx = abx; by = aby; cx = cax; cy = cay; }
+    else if (ch == 1) { ax = abx; ay = aby; cx = bcx; cy = bcy; }
+    else if (ch == 2) { ax = cax; ay = cay; bx = bcx; by = bcy; }
+    else { ax = bcx; ay = bcy; bx = cax; by = cay; cx = abx; cy = aby; }
+  }
+}
+
+template <int P>
+__device__ void near_flush(NearWarpSmem& W, int nleaf, int lane, const double* __restrict__ nx,
+                           const double* __restrict__ ny, const double* __restrict__ nw, int Ln,
+                           double X0, double Y0, double E1x, double E1y, double E2x, double E2y,
+                           double tx, double ty, double& acc) {
+  const int total = nleaf * Ln;
+  int li = lane / Ln, ni = lane - li * Ln;
+  for (int j = lane; j < total; j += 32) {
+    const double u = nx[ni], v = ny[ni];
+    const double xi = W.la[li] + (u * W.lc[li] + v * W.le[li]);
+    const double eta = W.lb[li] + (u * W.ld[li] + v * W.lf[li]);
+    const double yx = X0 + (xi * E1x + eta * E2x);
+    const double yy = Y0 + (xi * E1y + eta * E2y);
+    const double f = density<P>(W.cc, xi, eta);
+    const double dx = tx - yx, dy = ty - yy;
+    const double r2 = fma(dx, dx, dy * dy);
+    acc = fma(nw[ni] * W.ls[li], f * log(r2), acc);
+    ni += 32;
+    while (ni >= Ln) { ni -= Ln; ++li; }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(NEAR_WARPS * 32)
+    k_near(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
+           const double2* __restrict__ txy, const ElemRec* __restrict__ el,
+           const double* __restrict__ coeffs, const double* __restrict__ sx,
+           const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
+           double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ leaves_out,
+           unsigned long long* __restrict__ stats, int* __restrict__ err) {
+  constexpr int M = (P + 1) * (P + 2) / 2;
+  __shared__ NearWarpSmem Wsm[NEAR_WARPS];
+  __shared__ double snx[kMaxNearRule], sny[kMaxNearRule], snw[kMaxNearRule], skd[kMaxNearDepth + 2];
+  const int Ln = R->len_n, len_q = R->len_q;
+  for (int i = threadIdx.x; i < Ln; i += blockDim.x) {
+    snx[i] = R->near_x[i];
+    sny[i] = R->near_y[i];
+    snw[i] = R->near_w[i];
+  }
+  for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  NearWarpSmem& W = Wsm[wid];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned long long my_leaves = 0, my_rle1 = 0;
+  int my_maxd = 0;
+  for (int64_t p = (int64_t)blockIdx.x * NEAR_WARPS + wid; p < n_pairs;
+       p += (int64_t)gridDim.x * NEAR_WARPS) {
+    const int32_t t = pair_tgt[p], e = pair_elem[p];
+    const double2 tp = txy[t];
+    const double tx = tp.x, ty = tp.y;
+    const ElemRec& Er = el[e];
+    const double X0 = Er.x0, Y0 = Er.y0, E1x = Er.e1x, E1y = Er.e1y, E2x = Er.e2x, E2y = Er.e2y;
+    const double det = Er.det, rho0n = Er.rho0n;
+    for (int j = lane; j < M; j += 32) W.cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    if (lane == 0) {
+      W.fpath[0][0] = 0ull;
+      W.fdep[0][0] = 0;
+    }
+    __syncwarp();
+    int cur = 0, fcnt = 1, nleaf = 0;
+    double acc = 0.0;
+    long long pair_leaves = 0;
+    bool bad = false;
+    while (fcnt > 0 && !bad) {
+      int ncnt = 0;
+      for (int base = 0; base < fcnt; base += 32) {
+        const int i = base + lane;
+        const bool act = i < fcnt;
+        bool accept = false;
+        unsigned long long path = 0;
+        int d = 0;
+        double ax = 0, ay = 0, bx = 0, by = 0, cx = 0, cy = 0;
+        if (act) {
+          path = W.fpath[cur][i];
+          d = W.fdep[cur][i];
+          decode_path(path, d, ax, ay, bx, by, cx, cy);
+          const double rd = rn_mul(rho0n, skd[d]);
+          if (!(rd > 1.0)) {
+            accept = true;
+            ++my_rle1;
+          } else {
+            const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+            const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
+            double px[3], py[3], dist[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              px[k] = rn_add(X0, rn_add(rn_mul(vxs[k], E1x), rn_mul(vys[k], E2x)));
+              py[k] = rn_add(Y0, rn_add(rn_mul(vxs[k], E1y), rn_mul(vys[k], E2y)));
+              dist[k] = rn_dist(tx, ty, px[k], py[k]);
+            }
+            bool nearp = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              const int k1 = (k + 1) % 3;
+              const double len = rn_dist(px[k1], py[k1], px[k], py[k]);
+              if (rn_add(dist[k], dist[k1]) < rn_mul(g, len)) nearp = true;
+            }
+            accept = !nearp;
+          }
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, act && accept);
+        const unsigned rm = __ballot_sync(0xffffffffu, act && !accept);
+        const int na = __popc(am);
+        if (nleaf + na > LCAP) {
+          __syncwarp();
+          near_flush<P>(W, nleaf, lane, snx, sny, snw, Ln, X0, Y0, E1x, E1y, E2x, E2y, tx, ty, acc);
+          __syncwarp();
+          nleaf = 0;
+        }
+        if (act && accept) {
+          const int slot = nleaf + __popc(am & lt_mask);
+          W.la[slot] = ax;
+          W.lb[slot] = ay;
+          W.lc[slot] = bx - ax;
+          W.ld[slot] = by - ay;
+          W.le[slot] = cx - ax;
+          W.lf[slot] = cy - ay;
+          W.ls[slot] = det * ldexp(1.0, -2 * d) * kInv4Pi;
+          if (d > my_maxd) my_maxd = d;
+        }
+        nleaf += na;
+        pair_leaves += na;
+        if (act && !accept) {
+          const int slot = ncnt + 4 * __popc(rm & lt_mask);
+          if (d + 1 > kMaxPathDepth || slot + 3 >= FCAP) {
+            bad = true;
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              W.fpath[cur ^ 1][slot + c] = (path << 2) | (unsigned long long)c;
+              W.fdep[cur ^ 1][slot + c] = (unsigned char)(d + 1);
+            }
+          }
+        }
+        ncnt += 4 * __popc(rm);
+        bad = __any_sync(0xffffffffu, bad);
+      }
+      __syncwarp();
+      cur ^= 1;
+      fcnt = ncnt;
+    }
+    if (bad) {
+      if (lane == 0) atomicExch(err, 2);
+      nleaf = 0;
+    }
+    __syncwarp();
+    near_flush<P>(W, nleaf, lane, snx, sny, snw, Ln, X0, Y0, E1x, E1y, E2x, E2y, tx, ty, acc);
+    const double val = warp_sum(acc);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq);
+    if (lane == 0) {
+      corr[p] = val - sub;
+      if (sub_out) {
+        corr[p] = val;
+        sub_out[p] = sub;
+      }
+      if (leaves_out) leaves_out[p] = pair_leaves;
+    }
+    my_leaves += (lane == 0) ? (unsigned long long)pair_leaves : 0ull;
+    __syncwarp();
+  }
+  // my_rle1 counted per lane for accepted items; sum over the warp
+  unsigned long long r = my_rle1;
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  int md = my_maxd;
+  for (int o = 16; o > 0; o >>= 1) md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+  if (lane == 0) {
+    if (my_leaves) atomicAdd(&stats[0], my_leaves);
+    if (r) atomicAdd(&stats[1], r);
+    atomicMax((unsigned long long*)&stats[2], (unsigned long long)md);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: self_eval in radius-arc-length coordinates.
+constexpr int SELF_WARPS = 4;
+
+struct SelfGeom {
+  double Ax, Ay, ABx, ABy, L, h, st;
+  double Arx, Ary, BRx, BRy;
+  int N, Mr, npan;
+  bool degenerate;
+};
+
+__device__ __forceinline__ void self_geom(double tx, double ty, double Ax, double Ay, double Bx,
+                                          double By, SelfGeom& G) {
+  G.Ax = Ax;
+  G.Ay = Ay;
+  G.ABx = rn_sub(Bx, Ax);
+  G.ABy = rn_sub(By, Ay);
+  G.L = rn_sqrt(rn_add(rn_mul(G.ABx, G.ABx), rn_mul(G.ABy, G.ABy)));
+  const double vAx = rn_sub(tx, Ax), vAy = rn_sub(ty, Ay);
+  const double cr = rn_sub(rn_mul(G.ABx, vAy), rn_mul(G.ABy, vAx));
+  G.h = rn_div(fabs(cr), G.L);
+  G.degenerate = !(G.h > rn_mul(1e-13, G.L));
+  const double sp = rn_div(rn_add(rn_mul(vAx, G.ABx), rn_mul(vAy, G.ABy)), G.L);
+  G.st = fmin(fmax(sp, 0.0), G.L);
+  const double sl = rn_div(G.st, G.L);
+  const double gx = rn_add(Ax, rn_mul(sl, G.ABx)), gy = rn_add(Ay, rn_mul(sl, G.ABy));
+  const double dmin = rn_dist(tx, ty, gx, gy);
+  int N = 0;
+  for (double x = G.st; !(x < dmin) && N < 1100; x *= 0.5) ++N;
+  int Mr = 0;
+  for (double x = rn_sub(G.L, G.st); !(x < dmin) && Mr < 1100; x *= 0.5) ++Mr;
+  G.N = N;
+  G.Mr = Mr;
+  G.npan = N + Mr + 2;
+}
+
+// panel boundary b_i, i = 0 .. N+M+2
+__device__ __forceinline__ double self_bnd(const SelfGeom& G, int i) {
+  if (i == 0) return 0.0;
+  if (i <= G.N) return rn_sub(G.st, ldexp(G.st, -i));
+  if (i == G.N + 1) return G.st;
+  if (i <= G.N + G.Mr + 1) return rn_add(G.st, ldexp(rn_sub(G.L, G.st), -(G.Mr + 1 - (i - G.N - 1))));
+  return G.L;
+}
+
+template <int P>
+__global__ void __launch_bounds__(SELF_WARPS * 32)
+    k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
+           const double2* __restrict__ txy, const ElemRec* __restrict__ el,
+           const double* __restrict__ coeffs, const double* __restrict__ sx,
+           const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
+           double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ panels_out,
+           unsigned long long* __restrict__ stats) {
+  constexpr int M = (P + 1) * (P + 2) / 2;
+  __shared__ double scc[SELF_WARPS][kMaxModes];
+  __shared__ double sglx[kMaxGL], sglw[kMaxGL], sgr[kMaxGGQ], sgw[kMaxGGQ], sglr[kMaxGGQ];
+  const int NL = R->n_l, NG = R->n_g1, len_q = R->len_q;
+  for (int i = threadIdx.x; i < NL; i += blockDim.x) {
+    sglx[i] = R->gl_x[i];
+    sglw[i] = R->gl_w[i];
+  }
+  for (int i = threadIdx.x; i < NG; i += blockDim.x) {
+    sgr[i] = R->ggq_r[i];
+    sgw[i] = R->ggq_w[i] * R->ggq_r[i];
+    sglr[i] = R->ggq_lr[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* cc = scc[wid];
+  unsigned long long my_panels = 0, my_degen = 0;
+  for (int64_t it = (int64_t)blockIdx.x * SELF_WARPS + wid; it < n_items;
+       it += (int64_t)gridDim.x * SELF_WARPS) {
+    const int32_t t = item_tgt ? item_tgt[it] : (int32_t)it;
+    const int32_t e = item_elem[it];
+    if (e < 0) {
+      if (lane == 0) {
+        corr[it] = 0.0;
+        if (sub_out) sub_out[it] = 0.0;
+        if (panels_out) panels_out[it] = 0;
+      }
+      continue;
+    }
+    const double2 tp = txy[t];
+    const double tx = tp.x, ty = tp.y;
+    const ElemRec& Er = el[e];
+    double txi, teta;
+    rn_locate(Er, tx, ty, txi, teta);
+    for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    __syncwarp();
+    const double vx[3] = {Er.x0, Er.x1, Er.x2}, vy[3] = {Er.y0, Er.y1, Er.y2};
+    const double rx[3] = {0.0, 1.0, 0.0}, ry[3] = {0.0, 0.0, 1.0};
+    double acc = 0.0;
+    long long npan_item = 0;
+    for (int k = 0; k < 3; ++k) {
+      const int k1 = (k + 1) % 3;
+      SelfGeom G;
+      self_geom(tx, ty, vx[k], vy[k], vx[k1], vy[k1], G);
+      if (G.degenerate) {
+        ++my_degen;  // identical in every lane; counted once below
+        continue;
+      }
+      const double Arx = rx[k], Ary = ry[k], BRx = rx[k1] - rx[k], BRy = ry[k1] - ry[k];
+      const int nodes = G.npan * NL;
+      for (int j = lane; j < nodes; j += 32) {
+        const int pi = j / NL, gq = j - pi * NL;
+        const double s0 = self_bnd(G, pi), s1 = self_bnd(G, pi + 1);
+        if (!(s1 > s0)) continue;
+        const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
+        const double s = fma(half, sglx[gq], mid);
+        const double ws = half * sglw[gq];
+        const double sl = s / G.L;
+        const double px = fma(sl, G.ABx, G.Ax), py = fma(sl, G.ABy, G.Ay);
+        const double ddx = px - tx, ddy = py - ty;
+        const double lr0 = 0.5 * log(fma(ddx, ddx, ddy * ddy));
+        const double grx = fma(sl, BRx, Arx) - txi, gry = fma(sl, BRy, Ary) - teta;
+        double inner = 0.0;
+        for (int q = 0; q < NG; ++q) {
+          const double rj = sgr[q];
+          const double f = density<P>(cc, fma(rj, grx, txi), fma(rj, gry, teta));
+          inner = fma(sgw[q] * (lr0 + sglr[q]), f, inner);
+        }
+        acc = fma(ws * G.h, inner, acc);
+      }
+      for (int pi = 0; pi < G.npan; ++pi)
+        if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
+    }
+    const double val = warp_sum(acc) * kInv2Pi;
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq);
+    if (lane == 0) {
+      corr[it] = sub_out ? val : val - sub;
+      if (sub_out) sub_out[it] = sub;
+      if (panels_out) panels_out[it] = npan_item;
+      my_panels += (unsigned long long)npan_item;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (my_panels) atomicAdd(&stats[3], my_panels);
+  } else {
+    my_degen = 0;
+  }
+  if (lane == 0 && my_degen) atomicAdd(&stats[4], my_degen);
+}
+
+__global__ void k_assemble(int64_t T, const double* __restrict__ ufar, const int64_t* __restrict__ off,
+                           const double* __restrict__ corr, const double* __restrict__ corr_self,
+                           double* __restrict__ u) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  double s = ufar[t];
+  for (int64_t p = off[t]; p < off[t + 1]; ++p) s += corr[p];
+  s += corr_self[t];
+  u[t] = s;
+}
+
+__global__ void k_count_self(int64_t T, const int32_t* __restrict__ self,
+                             unsigned long long* __restrict__ stats) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = t < T && self[t] >= 0;
+  const unsigned b = __ballot_sync(0xffffffffu, in);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(&stats[5], (unsigned long long)__popc(b));
+}
+
+// ---------------------------------------------------------------------------
+// host side
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) cap = std::max<size_t>(bytes, 256);
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+double cn_lookup(int n) {  // SPEC.md:430-438; N < 12 clamped to C_12
+  static const int kn[6] = {12, 20, 25, 30, 40, 50};
+  static const double kc[6] = {12.0, 6.8, 3.0, 2.5, 2.0, 1.0};
+  if (n <= 12) return 12.0;
+  if (n >= 50) return 1.0;
+  for (int i = 0; i + 1 < 6; ++i) {
+    if (n == kn[i]) return kc[i];
+    if (n > kn[i] && n < kn[i + 1]) {
+      const double f = double(n - kn[i]) / double(kn[i + 1] - kn[i]);
+      return kc[i] + (kc[i + 1] - kc[i]) * f;
+    }
+  }
+  return 1.0;
+}
+
+double w_edge(int len, const double* x, const double* y, const double* w) {  // rules.hpp:44-54
+  std::vector<double> d(len);
+  for (int i = 0; i < len; ++i) d[i] = std::min({x[i], y[i], (1.0 - x[i] - y[i]) / std::sqrt(2.0)});
+  std::vector<double> s = d;
+  std::nth_element(s.begin(), s.begin() + s.size() / 2, s.end());
+  const double med = s[s.size() / 2];
+  double best = 0.0;
+  for (int i = 0; i < len; ++i)
+    if (d[i] < med) best = std::max(best, w[i]);
+  return best;
+}
+
+}  // namespace
+
+struct vp_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // mesh
+  int64_t n_vert = 0, n_tri = 0;
+  std::vector<double> h_vxy;
+  std::vector<int32_t> h_tri;
+  bool have_mesh = false, have_rules = false, have_density = false, sources_valid = false;
+  // rules
+  vp_rules rules{};
+  std::vector<double> h_rules_store;
+  RulesDev h_rd{};
+  DevBuf d_rules;
+  // elements
+  DevBuf d_el;
+  std::vector<int32_t> h_allnear;
+  DevBuf d_allnear;
+  GridDev grid{};
+  DevBuf d_cbeg, d_cend, d_celems;
+  // density
+  int p = -1, M = 0;
+  DevBuf d_coeffs, d_V;
+  // sources
+  DevBuf d_sx, d_sy, d_sq;
+  // per-evaluation scratch
+  DevBuf d_txy, d_u, d_ufar, d_part, d_self, d_cnt, d_off, d_ids, d_ptgt, d_corr, d_corr_self,
+      d_selfref, d_stats, d_err, d_tmp, d_sub, d_leaves, d_pelem;
+  cudaEvent_t ev[8] = {};
+  int last_launches = 0;
+};
+
+namespace {
+
+int set_err(vp_ctx* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+
+#define CUDA_TRY(ctx, x)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_err(ctx, 3, std::string("cuda: ") + cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Per-element records on the host with the oracle's operation order
+// (oracle/vp_oracle.cpp Setup::init): list predicates stay bit-exact.
+int build_elements(vp_ctx* c) {
+  const int64_t E = c->n_tri;
+  const vp_rules& r = c->rules;
+  const double we = w_edge(r.len_q, r.far_x, r.far_y, r.far_w);
+  const double wn = w_edge(r.len_n, r.near_x, r.near_y, r.near_w);
+  const double cq = cn_lookup(r.q), cnn = cn_lookup(r.n_n);
+  std::vector<ElemRec> h(E);
+  c->h_allnear.clear();
+  double gx0 = 1e300, gy0 = 1e300, gx1 = -1e300, gy1 = -1e300;
+  std::vector<double> ext;
+  ext.reserve(E);
+  for (int64_t e = 0; e < E; ++e) {
+    ElemRec& R = h[e];
+    std::memset(&R, 0, sizeof(R));
+    const int32_t* id = &c->h_tri[3 * e];
+    double px[3], py[3];
+    for (int k = 0; k < 3; ++k) {
+      px[k] = c->h_vxy[2 * id[k]];
+      py[k] = c->h_vxy[2 * id[k] + 1];
+    }
+    R.x0 = px[0]; R.y0 = py[0]; R.x1 = px[1]; R.y1 = py[1]; R.x2 = px[2]; R.y2 = py[2];
+    R.e1x = px[1] - px[0];
+    R.e1y = py[1] - py[0];
+    R.e2x = px[2] - px[0];
+    R.e2y = py[2] - py[0];
+    const double t1 = R.e1x * R.e2y;
+    const double t2 = R.e2x * R.e1y;
+    R.det = t1 - t2;
+    if (!(R.det > 0.0))
+      return set_err(c, 1, "set_mesh: triangle " + std::to_string(e) +
+                               " not counter-clockwise (invariant: det > 0)");
+    R.i00 = R.e2y / R.det;
+    R.i01 = -R.e2x / R.det;
+    R.i10 = -R.e1y / R.det;
+    R.i11 = R.e1x / R.det;
+    const double w = we * R.det;
+    const double den = r.eps * cq;
+    const double rho0 = std::pow(w / den, 1.0 / (double)r.q);
+    const double wnn = wn * R.det;
+    const double denn = r.eps * cnn;
+    R.rho0n = std::pow(wnn / denn, 1.0 / (double)r.n_n);
+    if (!(rho0 > 1.0)) {  // SPEC.md:444 all-near
+      R.ta0 = R.ta1 = R.ta2 = -1.0;
+      c->h_allnear.push_back((int32_t)e);
+      continue;
+    }
+    const double g = (rho0 + 1.0 / rho0) * 0.5;
+    double ta[3];
+    double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
+    for (int k = 0; k < 3; ++k) {
+      const int k1 = (k + 1) % 3;
+      const double dx = px[k1] - px[k], dy = py[k1] - py[k];
+      const double len = std::sqrt(dx * dx + dy * dy);
+      ta[k] = g * len;
+      const double mx = (px[k] + px[k1]) * 0.5, my = (py[k] + py[k1]) * 0.5;
+      const double rr = ta[k] * 0.5 * (1.0 + 1e-9) + 1e-300;
+      lox = std::min(lox, mx - rr); hix = std::max(hix, mx + rr);
+      loy = std::min(loy, my - rr); hiy = std::max(hiy, my + rr);
+    }
+    R.ta0 = ta[0]; R.ta1 = ta[1]; R.ta2 = ta[2];
+    R.bx0 = lox; R.by0 = loy; R.bx1 = hix; R.by1 = hiy;
+    gx0 = std::min(gx0, lox); gy0 = std::min(gy0, loy);
+    gx1 = std::max(gx1, hix); gy1 = std::max(gy1, hiy);
+    ext.push_back(std::max(hix - lox, hiy - loy));
+  }
+  CUDA_TRY(c, c->d_el.ensure(sizeof(ElemRec) * E));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_el.p, h.data(), sizeof(ElemRec) * E, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, c->d_allnear.ensure(sizeof(int32_t) * (c->h_allnear.size() + 1)));
+  if (!c->h_allnear.empty())
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_allnear.p, c->h_allnear.data(), sizeof(int32_t) * c->h_allnear.size(),
+                                cudaMemcpyHostToDevice, c->stream));
+  // uniform grid: cell = median near-field extent, capped at 2^24 cells
+  GridDev& G = c->grid;
+  if (ext.empty()) {
+    G.x0 = G.y0 = 0.0;
+    G.cs = 1.0;
+    G.nx = G.ny = 1;
+  } else {
+    std::nth_element(ext.begin(), ext.begin() + ext.size() / 2, ext.end());
+    double cs = ext[ext.size() / 2];
+    const double W = gx1 - gx0, H = gy1 - gy0;
+    if (!(cs > 0.0)) cs = std::max(W, H);
+    while ((W / cs + 1) * (H / cs + 1) > double(1 << 24)) cs *= 1.5;
+    G.x0 = gx0;
+    G.y0 = gy0;
+    G.cs = cs;
+    G.nx = std::max(1, (int)std::ceil(W / cs));
+    G.ny = std::max(1, (int)std::ceil(H / cs));
+  }
+  G.inv_cs = 1.0 / G.cs;
+  const int64_t ncell = (int64_t)G.nx * G.ny;
+  // bin on the device: count -> scan -> fill -> stable radix sort by cell
+  DevBuf cnt, off, keys, vals, keys2, vals2;
+  CUDA_TRY(c, cnt.ensure(sizeof(int64_t) * (E + 1)));
+  CUDA_TRY(c, off.ensure(sizeof(int64_t) * (E + 1)));
+  k_bin_count<<<nblk(E, 256), 256, 0, c->stream>>>(E, c->d_el.as<ElemRec>(), G, cnt.as<int64_t>());
+  CUDA_TRY(c, cudaMemsetAsync(cnt.as<int64_t>() + E, 0, sizeof(int64_t), c->stream));
+  size_t tmpb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, cnt.as<int64_t>(), off.as<int64_t>(), E + 1, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, cnt.as<int64_t>(), off.as<int64_t>(), E + 1, c->stream);
+  int64_t npairs = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&npairs, off.as<int64_t>() + E, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (npairs > (int64_t)INT32_MAX) return set_err(c, 1, "set_rules: element binning too large");
+  CUDA_TRY(c, keys.ensure(sizeof(int32_t) * (npairs + 1)));
+  CUDA_TRY(c, vals.ensure(sizeof(int32_t) * (npairs + 1)));
+  CUDA_TRY(c, keys2.ensure(sizeof(int32_t) * (npairs + 1)));
+  CUDA_TRY(c, c->d_celems.ensure(sizeof(int32_t) * (npairs + 1)));
+  k_bin_fill<<<nblk(E, 256), 256, 0, c->stream>>>(E, c->d_el.as<ElemRec>(), G, off.as<int64_t>(),
+                                                   keys.as<int32_t>(), vals.as<int32_t>());
+  int endbit = 1;
+  while ((1ll << endbit) < ncell) ++endbit;
+  tmpb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, keys.as<int32_t>(), keys2.as<int32_t>(),
+                                  vals.as<int32_t>(), c->d_celems.as<int32_t>(), (int)npairs, 0,
+                                  endbit, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->d_tmp.p, tmpb, keys.as<int32_t>(), keys2.as<int32_t>(),
+                                  vals.as<int32_t>(), c->d_celems.as<int32_t>(), (int)npairs, 0,
+                                  endbit, c->stream);
+  CUDA_TRY(c, c->d_cbeg.ensure(sizeof(int64_t) * ncell));
+  CUDA_TRY(c, c->d_cend.ensure(sizeof(int64_t) * ncell));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_cbeg.p, 0, sizeof(int64_t) * ncell, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_cend.p, 0, sizeof(int64_t) * ncell, c->stream));
+  if (npairs > 0)
+    k_cell_ranges<<<nblk(npairs, 256), 256, 0, c->stream>>>(npairs, keys2.as<int32_t>(),
+                                                             c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>());
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+template <int P>
+void launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
+                 double* corr, double* sub, int64_t* leaves) {
+  const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 64);
+  k_near<P><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
+      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, leaves,
+      c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+}
+
+template <int P>
+void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
+                 double* corr, double* sub, int64_t* panels) {
+  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
+  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
+      n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
+      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
+      c->d_stats.as<unsigned long long>());
+}
+
+#define VP_DISPATCH_P(p, F, ...)      \
+  switch (p) {                        \
+    case 0: F<0>(__VA_ARGS__); break;   \
+    case 1: F<1>(__VA_ARGS__); break;   \
+    case 2: F<2>(__VA_ARGS__); break;   \
+    case 3: F<3>(__VA_ARGS__); break;   \
+    case 4: F<4>(__VA_ARGS__); break;   \
+    case 5: F<5>(__VA_ARGS__); break;   \
+    case 6: F<6>(__VA_ARGS__); break;   \
+    case 7: F<7>(__VA_ARGS__); break;   \
+    case 8: F<8>(__VA_ARGS__); break;   \
+    case 9: F<9>(__VA_ARGS__); break;   \
+    case 10: F<10>(__VA_ARGS__); break; \
+    case 11: F<11>(__VA_ARGS__); break; \
+    case 12: F<12>(__VA_ARGS__); break; \
+    default: break;                     \
+  }
+
+int ensure_ready(vp_ctx* c, bool need_density) {
+  if (!c) return 1;
+  if (!c->have_mesh) return set_err(c, 1, "usage: vp_set_mesh must precede evaluation");
+  if (!c->have_rules) return set_err(c, 1, "usage: vp_set_rules must precede evaluation");
+  if (need_density && !c->have_density) return set_err(c, 1, "usage: vp_set_density must precede evaluation");
+  return 0;
+}
+
+int compute_sources(vp_ctx* c) {
+  if (c->sources_valid) return 0;
+  const int64_t S = c->n_tri * c->rules.len_q;
+  CUDA_TRY(c, c->d_sx.ensure(sizeof(double) * S));
+  CUDA_TRY(c, c->d_sy.ensure(sizeof(double) * S));
+  CUDA_TRY(c, c->d_sq.ensure(sizeof(double) * S));
+  k_sources<<<nblk(S, 256), 256, 0, c->stream>>>(c->n_tri, c->rules.len_q, c->M, c->d_el.as<ElemRec>(),
+                                                  c->d_coeffs.as<double>(), c->d_V.as<double>(),
+                                                  c->d_rules.as<RulesDev>(), c->d_sx.as<double>(),
+                                                  c->d_sy.as<double>(), c->d_sq.as<double>());
+  CUDA_TRY(c, cudaGetLastError());
+  c->sources_valid = true;
+  c->last_launches += 1;
+  return 0;
+}
+
+int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar) {
+  const int64_t S = c->n_tri * c->rules.len_q;
+  const int64_t tblocks = nblk(T, FAR_THREADS * FAR_R);
+  // split sources so the grid covers >= 4 waves of the SMs
+  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4LL * c->sm_count + tblocks - 1) / tblocks));
+  int64_t chunk = (S + nsplit - 1) / nsplit;
+  chunk = (chunk + FAR_TILE - 1) / FAR_TILE * FAR_TILE;
+  nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
+  CUDA_TRY(c, c->d_part.ensure(sizeof(double) * T * nsplit));
+  dim3 grid((unsigned)tblocks, (unsigned)nsplit);
+  k_far<<<grid, FAR_THREADS, 0, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                             c->d_sq.as<double>(), chunk, c->d_part.as<double>());
+  k_far_reduce<<<nblk(T, 256), 256, 0, c->stream>>>(T, nsplit, c->d_part.as<double>(), ufar);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches += 2;
+  return 0;
+}
+
+// list build into ctx buffers: self, cnt, off (T+1), ids, selfref
+int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
+  CUDA_TRY(c, c->d_self.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->d_cnt.ensure(sizeof(int64_t) * (T + 1)));
+  CUDA_TRY(c, c->d_off.ensure(sizeof(int64_t) * (T + 1)));
+  CUDA_TRY(c, c->d_selfref.ensure(sizeof(double2) * (T + 1)));
+  const GridDev G = c->grid;
+  const int nan = (int)c->h_allnear.size();
+  k_lists<false><<<nblk(T, 128), 128, 0, c->stream>>>(
+      T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
+      c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
+      c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>());
+  CUDA_TRY(c, cudaMemsetAsync(c->d_cnt.as<int64_t>() + T, 0, sizeof(int64_t), c->stream));
+  size_t tmpb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
+  int64_t n_ids = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&n_ids, c->d_off.as<int64_t>() + T, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, c->d_ids.ensure(sizeof(int32_t) * (n_ids + 1)));
+  k_lists<true><<<nblk(T, 128), 128, 0, c->stream>>>(
+      T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
+      c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr,
+      c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), nullptr);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches += 3;
+  *n_ids_out = n_ids;
+  return 0;
+}
+
+int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats* st) {
+  c->last_launches = 0;
+  CUDA_TRY(c, c->d_stats.ensure(sizeof(unsigned long long) * 8));
+  CUDA_TRY(c, c->d_err.ensure(sizeof(int)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, sizeof(int), c->stream));
+  cudaEvent_t* ev = c->ev;
+  CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
+  int64_t n_ids = 0;
+  if (int rc = build_lists(c, T, txy, &n_ids)) return rc;
+  CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
+  c->sources_valid = false;  // strengths are part of every evaluation pass
+  if (int rc = compute_sources(c)) return rc;
+  CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * (T + 1)));
+  if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>())) return rc;
+  CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+  CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * (n_ids + 1)));
+  CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * (n_ids + 1)));
+  if (n_ids > 0) {
+    k_pair_tgt<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), c->d_ptgt.as<int32_t>());
+    VP_DISPATCH_P(c->p, launch_near, c, n_ids, c->d_ptgt.as<int32_t>(), c->d_ids.as<int32_t>(), txy,
+                  c->d_corr.as<double>(), nullptr, nullptr);
+    c->last_launches += 2;
+  }
+  CUDA_TRY(c, cudaEventRecord(ev[3], c->stream));
+  CUDA_TRY(c, c->d_corr_self.ensure(sizeof(double) * (T + 1)));
+  VP_DISPATCH_P(c->p, launch_self, c, T, nullptr, c->d_self.as<int32_t>(), txy, c->d_corr_self.as<double>(),
+                nullptr, nullptr);
+  c->last_launches += 1;
+  CUDA_TRY(c, cudaEventRecord(ev[4], c->stream));
+  k_assemble<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_ufar.as<double>(), c->d_off.as<int64_t>(),
+                                                   c->d_corr.as<double>(), c->d_corr_self.as<double>(), u);
+  k_count_self<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_self.as<int32_t>(), c->d_stats.as<unsigned long long>());
+  c->last_launches += 2;
+  CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
+  CUDA_TRY(c, cudaGetLastError());
+  unsigned long long hs[8];
+  int herr = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(hs, c->d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&herr, c->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (herr) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits "
+                                 "(target effectively on element boundary)");
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->n_targets = T;
+    st->n_near_pairs = n_ids;
+    st->n_leaves = (int64_t)hs[0];
+    st->n_rho_le1 = (int64_t)hs[1];
+    st->max_depth = (int32_t)hs[2];
+    st->n_panels = (int64_t)hs[3];
+    st->n_degenerate = (int64_t)hs[4];
+    st->n_self = (int64_t)hs[5];
+    st->n_outside = T - st->n_self;
+    st->n_sources = c->n_tri * c->rules.len_q;
+    st->gpu_launches = c->last_launches;
+    float ms[5];
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+    st->t_list_ms = ms[0];
+    st->t_far_ms = ms[1];
+    st->t_near_ms = ms[2];
+    st->t_self_ms = ms[3];
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev[0], ev[5]);
+    st->t_total_ms = tot;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+extern "C" {
+
+const char* vp_last_error(const vp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int vp_create(int device, vp_ctx** out) {
+  if (!out) return 1;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return 3;
+  }
+  if (device < 0 || device >= n) return 1;
+  if (cudaSetDevice(device) != cudaSuccess) return 3;
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 3;
+  if (prop.major < 10) return 3;  // sm_100a build only
+  vp_ctx* c = new vp_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return 3;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  double cn[kMaxModes];
+  for (int n2 = 0; n2 <= kMaxPdev; ++n2)
+    for (int m = 0; m <= n2; ++m) cn[koorn_index(m, n2)] = std::sqrt((double)((2 * m + 1) * (2 * n2 + 2)));
+  if (cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess) {
+    vp_destroy(c);
+    return 3;
+  }
+  *out = c;
+  return 0;
+}
+
+void vp_destroy(vp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int vp_device_info(vp_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!c) return 1;
+  cudaDeviceProp prop{};
+  CUDA_TRY(c, cudaGetDeviceProperties(&prop, c->device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return 0;
+}
+
+int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri) {
+  if (!c) return 1;
+  if (n_vert <= 0 || n_tri <= 0 || !vxy || !tri)
+    return set_err(c, 1, "set_mesh: empty mesh (invariant: n_vert > 0, n_tri > 0)");
+  if (n_tri > (int64_t)INT32_MAX / 4) return set_err(c, 1, "set_mesh: too many triangles");
+  for (int64_t i = 0; i < 3 * n_tri; ++i)
+    if (tri[i] < 0 || tri[i] >= n_vert) return set_err(c, 1, "set_mesh: triangle vertex index out of range");
+  for (int64_t i = 0; i < 2 * n_vert; ++i)
+    if (!std::isfinite(vxy[i])) return set_err(c, 2, "set_mesh: non-finite vertex coordinate");
+  c->h_vxy.assign(vxy, vxy + 2 * n_vert);
+  c->h_tri.assign(tri, tri + 3 * n_tri);
+  c->n_vert = n_vert;
+  c->n_tri = n_tri;
+  c->have_mesh = true;
+  c->sources_valid = false;
+  // triangle orientation is validated here so errors surface early
+  for (int64_t e = 0; e < n_tri; ++e) {
+    const int32_t* id = &tri[3 * e];
+    const double e1x = vxy[2 * id[1]] - vxy[2 * id[0]], e1y = vxy[2 * id[1] + 1] - vxy[2 * id[0] + 1];
+    const double e2x = vxy[2 * id[2]] - vxy[2 * id[0]], e2y = vxy[2 * id[2] + 1] - vxy[2 * id[0] + 1];
+    const double t1 = e1x * e2y, t2 = e2x * e1y;
+    if (!(t1 - t2 > 0.0)) {
+      c->have_mesh = false;
+      return set_err(c, 1, "set_mesh: triangle " + std::to_string(e) + " not counter-clockwise (invariant: det > 0)");
+    }
+  }
+  if (c->have_rules) {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (int rc = build_elements(c)) return rc;
+  }
+  if (c->have_density && c->M > 0) c->have_density = false;  // coefficients are per triangle
+  return 0;
+}
+
+int vp_set_rules(vp_ctx* c, const vp_rules* r) {
+  if (!c) return 1;
+  if (!r) return set_err(c, 1, "set_rules: null rules");
+  if (r->len_q <= 0 || r->len_q > kMaxFar || !r->far_x || !r->far_y || !r->far_w)
+    return set_err(c, 1, "set_rules: far rule length must be in [1, 512]");
+  if (r->len_n <= 0 || r->len_n > kMaxNearRule || !r->near_x || !r->near_y || !r->near_w)
+    return set_err(c, 1, "set_rules: near rule length must be in [1, 256]");
+  if (r->n_l <= 0 || r->n_l > kMaxGL || !r->gl_x || !r->gl_w)
+    return set_err(c, 1, "set_rules: Gauss-Legendre length must be in [1, 64]");
+  if (r->n_g < 0 || r->n_g + 1 > kMaxGGQ || !r->ggq_r || !r->ggq_w)
+    return set_err(c, 1, "set_rules: GGQ order must be in [0, 31]");
+  if (!(r->eps > 0.0) || r->q < 1 || r->n_n < 1) return set_err(c, 1, "set_rules: eps > 0, q >= 1, n_n >= 1 required");
+  for (int i = 0; i < r->len_q; ++i)
+    if (!(r->far_w[i] > 0.0)) return set_err(c, 2, "rule table: non-positive weight (invariant: weights > 0)");
+  for (int i = 0; i <= r->n_g; ++i)
+    if (!(r->ggq_r[i] > 0.0 && r->ggq_r[i] < 1.0)) return set_err(c, 2, "set_rules: GGQ nodes must lie in (0,1)");
+  // keep host copies (the vp_rules pointers are caller-owned)
+  std::vector<double>& st = c->h_rules_store;
+  st.clear();
+  auto keep = [&](const double* p, int n) {
+    const size_t o = st.size();
+    st.insert(st.end(), p, p + n);
+    return o;
+  };
+  const size_t o1 = keep(r->far_x, r->len_q), o2 = keep(r->far_y, r->len_q), o3 = keep(r->far_w, r->len_q);
+  const size_t o4 = keep(r->near_x, r->len_n), o5 = keep(r->near_y, r->len_n), o6 = keep(r->near_w, r->len_n);
+  const size_t o7 = keep(r->gl_x, r->n_l), o8 = keep(r->gl_w, r->n_l);
+  const size_t o9 = keep(r->ggq_r, r->n_g + 1), o10 = keep(r->ggq_w, r->n_g + 1);
+  c->rules = *r;
+  c->rules.far_x = &st[o1]; c->rules.far_y = &st[o2]; c->rules.far_w = &st[o3];
+  c->rules.near_x = &st[o4]; c->rules.near_y = &st[o5]; c->rules.near_w = &st[o6];
+  c->rules.gl_x = &st[o7]; c->rules.gl_w = &st[o8];
+  c->rules.ggq_r = &st[o9]; c->rules.ggq_w = &st[o10];
+  RulesDev& d = c->h_rd;
+  std::memset(&d, 0, sizeof(d));
+  d.len_q = r->len_q; d.len_n = r->len_n; d.n_l = r->n_l; d.n_g1 = r->n_g + 1; d.n_n = r->n_n; d.q = r->q;
+  for (int i = 0; i < r->len_q; ++i) { d.far_x[i] = r->far_x[i]; d.far_y[i] = r->far_y[i]; d.far_w[i] = r->far_w[i]; }
+  for (int i = 0; i < r->len_n; ++i) { d.near_x[i] = r->near_x[i]; d.near_y[i] = r->near_y[i]; d.near_w[i] = r->near_w[i]; }
+  for (int i = 0; i < r->n_l; ++i) { d.gl_x[i] = r->gl_x[i]; d.gl_w[i] = r->gl_w[i]; }
+  for (int i = 0; i <= r->n_g; ++i) { d.ggq_r[i] = r->ggq_r[i]; d.ggq_w[i] = r->ggq_w[i]; d.ggq_lr[i] = std::log(r->ggq_r[i]); }
+  for (int k = 0; k <= kMaxNearDepth + 1; ++k) d.kd[k] = std::pow(4.0, -(double)k / (double)r->n_n);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, c->d_rules.ensure(sizeof(RulesDev)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_rules.p, &d, sizeof(RulesDev), cudaMemcpyHostToDevice, c->stream));
+  c->have_rules = true;
+  c->sources_valid = false;
+  if (c->have_mesh)
+    if (int rc = build_elements(c)) return rc;
+  if (c->p >= 0) {  // Koornwinder values at the far nodes for K1
+    const int M = koorn_size(c->p);
+    std::vector<double> V((size_t)r->len_q * M);
+    for (int i = 0; i < r->len_q; ++i) koorn_eval(c->p, r->far_x[i], r->far_y[i], &V[(size_t)i * M]);
+    CUDA_TRY(c, c->d_V.ensure(sizeof(double) * V.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_V.p, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return 0;
+}
+
+int vp_set_density(vp_ctx* c, int p, const double* coeffs) {
+  if (!c) return 1;
+  if (!c->have_mesh) return set_err(c, 1, "usage: vp_set_mesh must precede vp_set_density");
+  if (p < 0 || p > kMaxPdev) return set_err(c, 1, "set_density: order p must be in [0, 12]");
+  if (!coeffs) return set_err(c, 1, "set_density: null coefficients");
+  const int M = koorn_size(p);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, c->d_coeffs.ensure(sizeof(double) * c->n_tri * M));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_coeffs.p, coeffs, sizeof(double) * c->n_tri * M, cudaMemcpyHostToDevice, c->stream));
+  c->p = p;
+  c->M = M;
+  if (c->have_rules) {
+    const vp_rules& r = c->rules;
+    std::vector<double> V((size_t)r.len_q * M);
+    for (int i = 0; i < r.len_q; ++i) koorn_eval(p, r.far_x[i], r.far_y[i], &V[(size_t)i * M]);
+    CUDA_TRY(c, c->d_V.ensure(sizeof(double) * V.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_V.p, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->have_density = true;
+  c->sources_valid = false;
+  return 0;
+}
+
+int vp_build_nearlist(vp_ctx* c, int64_t n_tgt, const double* txy, int32_t* self_out, int64_t* offsets_out,
+                      int32_t* ids_out, int64_t ids_cap, int64_t* n_ids) {
+  if (int rc = ensure_ready(c, false)) return rc;
+  if (n_tgt < 0 || (n_tgt > 0 && !txy)) return set_err(c, 1, "nearlist: bad target array");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (n_tgt == 0) {
+    if (offsets_out) offsets_out[0] = 0;
+    if (n_ids) *n_ids = 0;
+    return 0;
+  }
+  CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n_tgt));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n_tgt, cudaMemcpyHostToDevice, c->stream));
+  int64_t nids = 0;
+  if (int rc = build_lists(c, n_tgt, c->d_txy.as<double2>(), &nids)) return rc;
+  if (n_ids) *n_ids = nids;
+  if (self_out)
+    CUDA_TRY(c, cudaMemcpyAsync(self_out, c->d_self.p, sizeof(int32_t) * n_tgt, cudaMemcpyDeviceToHost, c->stream));
+  if (offsets_out)
+    CUDA_TRY(c, cudaMemcpyAsync(offsets_out, c->d_off.p, sizeof(int64_t) * (n_tgt + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (ids_out) {
+    if (nids > ids_cap) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      return set_err(c, 1, "nearlist: ids capacity too small");
+    }
+    if (nids > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(ids_out, c->d_ids.p, sizeof(int32_t) * nids, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vp_evaluate_device(vp_ctx* c, int64_t n_tgt, const double* d_txy, double* d_u, void* stream, vp_stats* st) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  if (n_tgt < 0 || (n_tgt > 0 && (!d_txy || !d_u))) return set_err(c, 1, "evaluate: bad target array");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (n_tgt == 0) {
+    if (st) std::memset(st, 0, sizeof(*st));
+    return 0;
+  }
+  cudaStream_t user = (cudaStream_t)stream;
+  if (user) {  // order against the caller's stream
+    cudaEvent_t e;
+    CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEventRecord(e, user);
+    cudaStreamWaitEvent(c->stream, e, 0);
+    cudaEventDestroy(e);
+  }
+  const int rc = evaluate_impl(c, n_tgt, (const double2*)d_txy, d_u, st);
+  return rc;
+}
+
+int vp_evaluate(vp_ctx* c, int64_t n_tgt, const double* txy, double* u_out, vp_stats* st) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  if (n_tgt < 0 || (n_tgt > 0 && (!txy || !u_out))) return set_err(c, 1, "evaluate: bad target array");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (n_tgt == 0) {
+    if (st) std::memset(st, 0, sizeof(*st));
+    return 0;
+  }
+  for (int64_t i = 0; i < 2 * n_tgt; ++i)
+    if (!std::isfinite(txy[i])) return set_err(c, 2, "evaluate: non-finite target coordinate");
+  CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n_tgt));
+  CUDA_TRY(c, c->d_u.ensure(sizeof(double) * n_tgt));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n_tgt, cudaMemcpyHostToDevice, c->stream));
+  if (int rc = evaluate_impl(c, n_tgt, c->d_txy.as<double2>(), c->d_u.as<double>(), st)) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(u_out, c->d_u.p, sizeof(double) * n_tgt, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vp_far_field(vp_ctx* c, int64_t n_tgt, const double* txy, double* u_far) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  if (n_tgt <= 0 || !txy || !u_far) return set_err(c, 1, "far_field: bad target array");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n_tgt));
+  CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * n_tgt));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n_tgt, cudaMemcpyHostToDevice, c->stream));
+  if (int rc = compute_sources(c)) return rc;
+  if (int rc = far_sum(c, n_tgt, c->d_txy.as<double2>(), c->d_ufar.as<double>())) return rc;
+  CUDA_TRY(c, cudaMemcpyAsync(u_far, c->d_ufar.p, sizeof(double) * n_tgt, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int vp_sources(vp_ctx* c, double* sx, double* sy, double* q) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (int rc = compute_sources(c)) return rc;
+  const size_t n = sizeof(double) * c->n_tri * c->rules.len_q;
+  if (sx) CUDA_TRY(c, cudaMemcpyAsync(sx, c->d_sx.p, n, cudaMemcpyDeviceToHost, c->stream));
+  if (sy) CUDA_TRY(c, cudaMemcpyAsync(sy, c->d_sy.p, n, cudaMemcpyDeviceToHost, c->stream));
+  if (q) CUDA_TRY(c, cudaMemcpyAsync(q, c->d_sq.p, n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+static int pairs_common(vp_ctx* c, int64_t n, const double* txy, const int32_t* elem, bool self,
+                        double* val, double* sub, int64_t* cnt) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  if (n <= 0 || !txy || !elem || !val) return set_err(c, 1, "pairs: bad arrays");
+  for (int64_t i = 0; i < n; ++i)
+    if (elem[i] < 0 || elem[i] >= c->n_tri) return set_err(c, 1, "pairs: element out of range");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (int rc = compute_sources(c)) return rc;
+  CUDA_TRY(c, c->d_stats.ensure(sizeof(unsigned long long) * 8));
+  CUDA_TRY(c, c->d_err.ensure(sizeof(int)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n));
+  CUDA_TRY(c, c->d_pelem.ensure(sizeof(int32_t) * n));
+  CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * n));
+  CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * n));
+  CUDA_TRY(c, c->d_sub.ensure(sizeof(double) * n));
+  CUDA_TRY(c, c->d_leaves.ensure(sizeof(int64_t) * n));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_pelem.p, elem, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  std::vector<int32_t> idx(n);
+  for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_ptgt.p, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  if (self) {
+    VP_DISPATCH_P(c->p, launch_self, c, n, c->d_ptgt.as<int32_t>(), c->d_pelem.as<int32_t>(),
+                  c->d_txy.as<double2>(), c->d_corr.as<double>(), c->d_sub.as<double>(), c->d_leaves.as<int64_t>());
+  } else {
+    VP_DISPATCH_P(c->p, launch_near, c, n, c->d_ptgt.as<int32_t>(), c->d_pelem.as<int32_t>(),
+                  c->d_txy.as<double2>(), c->d_corr.as<double>(), c->d_sub.as<double>(), c->d_leaves.as<int64_t>());
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  int herr = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(val, c->d_corr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (sub) CUDA_TRY(c, cudaMemcpyAsync(sub, c->d_sub.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  if (cnt) CUDA_TRY(c, cudaMemcpyAsync(cnt, c->d_leaves.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&herr, c->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (herr) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits");
+  return 0;
+}
+
+int vp_near_pairs(vp_ctx* c, int64_t n, const double* txy, const int32_t* elem, double* val, double* sub,
+                  int64_t* leaves) {
+  return pairs_common(c, n, txy, elem, false, val, sub, leaves);
+}
+
+int vp_self_pairs(vp_ctx* c, int64_t n, const double* txy, const int32_t* elem, double* val, double* sub,
+                  int64_t* panels) {
+  return pairs_common(c, n, txy, elem, true, val, sub, panels);
+}
+
+}  // extern "C"
