@@ -70,6 +70,8 @@ typedef struct {
   double t_near_ms;     /* device time: near pairs (K4): T_N */
   double t_self_ms;     /* device time: self pairs (K5): T_S */
   double t_total_ms;    /* device time of the whole evaluation */
+  double t_sources_ms;  /* device time of K1 alone */
+  double t_far_kernel_ms; /* device time of K2 (far sum + its fixed-order reduction) */
 } vp_stats;
 
 /* context (device = CUDA ordinal) */
@@ -125,8 +127,7 @@ int vp_near_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
 int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t* elem,
                   double* val, double* sub, int64_t* panels);
 
-/* Roofline bookkeeping for the bench: device time of the last far-field
- * kernel launch sequence and its launch count. */
+/* SM count and compute capability of the context's device. */
 int vp_device_info(vp_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 
 #ifdef __cplusplus

@@ -64,9 +64,28 @@ def lib():
     global _lib
     if _lib is None:
         L = ctypes.CDLL(ORACLE_PATH)
-        L.vpo_last_error.restype = ctypes.c_char_p
-        L.vpo_cn_lookup.restype = ctypes.c_double
-        L.vpo_w_edge.restype = ctypes.c_double
+        P = ctypes.POINTER(VpoProblem)
+        i64, i32, dbl, vp_ = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+        sigs = {
+            "vpo_last_error": (ctypes.c_char_p, []),
+            "vpo_cn_lookup": (dbl, [i32]),
+            "vpo_w_edge": (dbl, [i32, _d_p, _d_p, _d_p]),
+            "vpo_koornwinder": (i32, [i32, dbl, dbl, _d_p]),
+            "vpo_validate_rule": (i32, [i32, i32, _d_p, _d_p, _d_p]),
+            "vpo_gauss_legendre": (i32, [i32, _d_p, _d_p]),
+            "vpo_quadtree_query": (i32, [i64, _d_p, i32, dbl, dbl, dbl, dbl, _i32_p, i64, _i64_p, _i64_p]),
+            "vpo_element_models": (i32, [P, _d_p, _d_p, _d_p]),
+            "vpo_nearlist": (i32, [P, i64, _d_p, _i32_p, _i64_p, _i32_p, i64, _i64_p]),
+            "vpo_sources": (i32, [P, _d_p, _d_p, _d_p]),
+            "vpo_far_sum": (i32, [P, i64, _d_p, i32, _d_p]),
+            "vpo_near_pair": (i32, [P, dbl, dbl, ctypes.c_int32, _d_p, _d_p, _i64_p, ctypes.POINTER(ctypes.c_int32)]),
+            "vpo_self": (i32, [P, dbl, dbl, ctypes.c_int32, _d_p, _d_p, _i64_p]),
+            "vpo_evaluate": (i32, [P, i64, _d_p, i32, _d_p, _d_p, ctypes.POINTER(VpoStats)]),
+        }
+        for name, (res, args) in sigs.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
         _lib = L
     return _lib
 
@@ -75,7 +94,14 @@ def ref():
     """The reference's own headers behind an extern "C" shim (None if not built)."""
     global _ref
     if _ref is None and os.path.exists(REF_PATH):
-        _ref = ctypes.CDLL(REF_PATH)
+        R = ctypes.CDLL(REF_PATH)
+        i64, i32, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        R.vpref_koornwinder.argtypes = [i32, dbl, dbl, _d_p]
+        R.vpref_gauss_legendre.argtypes = [i32, _d_p, _d_p]
+        R.vpref_quadtree_query.argtypes = [i64, _d_p, i32, dbl, dbl, dbl, dbl, _i32_p, i64, _i64_p, _i64_p]
+        for f in (R.vpref_koornwinder, R.vpref_gauss_legendre, R.vpref_quadtree_query):
+            f.restype = i32
+        _ref = R
     return _ref
 
 
@@ -194,7 +220,7 @@ def quadtree_query(pts, leaf_cap, rect, use_ref=False):
     vis = ctypes.c_int64()
     L = ref() if use_ref else lib()
     fn = L.vpref_quadtree_query if use_ref else L.vpo_quadtree_query
-    args = [pts.shape[0], _d(pts), leaf_cap] + [ctypes.c_double(v) for v in rect]
+    args = [pts.shape[0], _d(pts), leaf_cap] + [float(v) for v in rect]
     rc = fn(*args, None, 0, ctypes.byref(n), ctypes.byref(vis))
     if rc:
         raise OracleError(rc, "quadtree query failed")

@@ -176,12 +176,17 @@ struct QTree {
     split(0, std::move(all));
   }
   void split(size_t ni, std::vector<int> items) {
-    if ((int)items.size() <= cap || diam(nodes[ni]) < min_diam) {
+    const Node box = nodes[ni];
+    const double cx = (box.lox + box.hix) * 0.5, cy = (box.loy + box.hiy) * 0.5;
+    // Deviation (documented in DESIGN.md): also stop when the box can no
+    // longer be halved in floating point.  With every point coincident the
+    // root box is degenerate, min_diam falls below the fp spacing and the
+    // reference's subdivide (quadtree.hpp:79-109) recurses without end.
+    const bool unsplittable = !(cx > box.lox && cx < box.hix) && !(cy > box.loy && cy < box.hiy);
+    if ((int)items.size() <= cap || diam(box) < min_diam || unsplittable) {
       nodes[ni].items = std::move(items);
       return;
     }
-    const Node box = nodes[ni];
-    const double cx = (box.lox + box.hix) * 0.5, cy = (box.loy + box.hiy) * 0.5;
     std::vector<int> b[4];
     for (int idx : items) {
       const int qd = (pts[2 * idx] >= cx ? 1 : 0) + (pts[2 * idx + 1] >= cy ? 2 : 0);

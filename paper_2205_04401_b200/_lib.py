@@ -40,7 +40,8 @@ class VpStats(ctypes.Structure):
         ("max_depth", ctypes.c_int32), ("gpu_launches", ctypes.c_int32),
         ("t_list_ms", ctypes.c_double), ("t_far_ms", ctypes.c_double),
         ("t_near_ms", ctypes.c_double), ("t_self_ms", ctypes.c_double),
-        ("t_total_ms", ctypes.c_double),
+        ("t_total_ms", ctypes.c_double), ("t_sources_ms", ctypes.c_double),
+        ("t_far_kernel_ms", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -997,6 +997,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   CUDA_TRY(c, cudaEventRecord(ev[1], c->stream));
   c->sources_valid = false;  // strengths are part of every evaluation pass
   if (int rc = compute_sources(c)) return rc;
+  CUDA_TRY(c, cudaEventRecord(ev[6], c->stream));
   CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * (T + 1)));
   if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>())) return rc;
   CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
@@ -1043,6 +1044,11 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     float ms[5];
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
     st->t_list_ms = ms[0];
+    float msrc = 0, mfar = 0;
+    cudaEventElapsedTime(&msrc, ev[1], ev[6]);
+    cudaEventElapsedTime(&mfar, ev[6], ev[2]);
+    st->t_sources_ms = msrc;
+    st->t_far_kernel_ms = mfar;
     st->t_far_ms = ms[1];
     st->t_near_ms = ms[2];
     st->t_self_ms = ms[3];

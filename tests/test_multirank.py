@@ -1,0 +1,65 @@
+"""Multi-rank host logic on CPU with the gloo backend (world_size 2).
+
+On B200 boxes each rank drives its own GPU and the collective is NCCL; the
+sharding and gather code is the same.  Per-target results are independent,
+so the gathered u must be bit-identical to the single-process result."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2205_04401_b200.dist import gather_potentials, morton_order, padded_shard, shard_bounds
+
+
+def test_shard_bounds_partition():
+    for n in (0, 1, 7, 100, 184320):
+        for world in (1, 2, 3, 4, 8):
+            b = [shard_bounds(n, r, world) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in b]
+            assert max(sizes) - min(sizes) <= 1 and max(sizes) <= padded_shard(n, world)
+
+
+def test_morton_order_is_permutation():
+    t = np.random.default_rng(0).random((1000, 2))
+    o = morton_order(t)
+    assert np.array_equal(np.sort(o), np.arange(1000))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2205_04401_b200 as vp
+    from oracle.binding import Oracle
+    pr = vp.load_config(1)
+    txy = pr.txy[::3]
+    lo, hi = shard_bounds(len(txy), rank, world)
+    u, _, _ = Oracle.from_problem(pr).evaluate(txy[lo:hi], nthreads=2)
+    full = gather_potentials(torch.from_numpy(u), len(txy), rank, world)
+    if rank == 0:
+        np.save(out, full.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_gloo_two_rank_gather_is_bit_identical(tmp_path):
+    out = str(tmp_path / "u.npy")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    import paper_2205_04401_b200 as vp
+    from oracle.binding import Oracle
+    pr = vp.load_config(1)
+    u1, _, _ = Oracle.from_problem(pr).evaluate(pr.txy[::3], nthreads=2)
+    assert np.array_equal(np.load(out), u1)
