@@ -198,15 +198,20 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 // targets; each thread keeps FAR_R targets in registers.  The source range
 // is split over gridDim.y; partials are reduced in fixed order.
 constexpr int FAR_THREADS = 256;
-constexpr int FAR_R = 4;
-constexpr int FAR_TILE = 512;
+constexpr int FAR_R = 8;
+constexpr int FAR_TILE = 256;
 
-__global__ void __launch_bounds__(FAR_THREADS) k_far(int64_t T, const double2* __restrict__ txy,
-                                                     int64_t S, const double* __restrict__ sx,
-                                                     const double* __restrict__ sy,
-                                                     const double* __restrict__ sq, int64_t chunk,
-                                                     double* __restrict__ part) {
-  __shared__ double shx[FAR_TILE], shy[FAR_TILE], shq[FAR_TILE];
+__device__ double2 g_logtab[kLogEntries];  // {r_k, -log r_k}, filled at vp_create
+
+__global__ void __launch_bounds__(FAR_THREADS, 2)
+    k_far(int64_t T, const double2* __restrict__ txy, int64_t S, const double* __restrict__ sx,
+          const double* __restrict__ sy, const double* __restrict__ sq, int64_t chunk,
+          double* __restrict__ part) {
+  __shared__ LogTab tab;
+  __shared__ double2 sxy[FAR_TILE];
+  __shared__ double ssq[FAR_TILE];
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += FAR_THREADS) tab.e[i] = g_logtab[i / kLogCopies];
+  const double2* lbase = tab.e + (threadIdx.x & (kLogCopies - 1));
   const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
   double tx[FAR_R], ty[FAR_R], acc[FAR_R];
 #pragma unroll
@@ -222,20 +227,20 @@ __global__ void __launch_bounds__(FAR_THREADS) k_far(int64_t T, const double2* _
   for (int64_t base = s0; base < s1; base += FAR_TILE) {
     const int n = (int)min((int64_t)FAR_TILE, s1 - base);
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += FAR_THREADS) {
-      shx[j] = sx[base + j];
-      shy[j] = sy[base + j];
-      shq[j] = sq[base + j];
+    if (threadIdx.x < n) {
+      sxy[threadIdx.x] = make_double2(sx[base + threadIdx.x], sy[base + threadIdx.x]);
+      ssq[threadIdx.x] = sq[base + threadIdx.x];
     }
     __syncthreads();
+#pragma unroll 2
     for (int j = 0; j < n; ++j) {
-      const double px = shx[j], py = shy[j], q = shq[j];
+      const double2 ps = sxy[j];
+      const double q = ssq[j];
 #pragma unroll
       for (int r = 0; r < FAR_R; ++r) {
-        const double dx = tx[r] - px, dy = ty[r] - py;
+        const double dx = tx[r] - ps.x, dy = ty[r] - ps.y;
         const double r2 = fma(dx, dx, dy * dy);
-        const double lg = r2 > 0.0 ? log(r2) : 0.0;
-        acc[r] = fma(q, lg, acc[r]);
+        acc[r] = fma(q, fast_log_r2<kLogCopies>(lbase, r2), acc[r]);
       }
     }
   }
@@ -259,32 +264,31 @@ __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ p
 __device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q, double tx,
                                                  double ty, const double* __restrict__ sx,
                                                  const double* __restrict__ sy,
-                                                 const double* __restrict__ sq) {
+                                                 const double* __restrict__ sq,
+                                                 const double2* __restrict__ ltab) {
   double s = 0.0;
   for (int i = lane; i < len_q; i += 32) {
     const int64_t k = e * len_q + i;
     const double dx = tx - sx[k], dy = ty - sy[k];
     const double r2 = fma(dx, dx, dy * dy);
-    if (r2 > 0.0) s = fma(sq[k], log(r2), s);
+    s = fma(sq[k], fast_log_r2<1>(ltab, r2), s);
   }
   return warp_sum(s);
 }
 
 // ---------------------------------------------------------------------------
-// K4: near_eval over a warp-cooperative level-synchronous subdivision.
-// Sub-simplices are coded by their 2-bit child path; accepted leaves are
-// buffered and integrated lane-parallel over (leaf, node).
-constexpr int NEAR_WARPS = 4;
-constexpr int FCAP = 128;
-constexpr int LCAP = 64;
-constexpr int kMaxPathDepth = 31;
-
-struct NearWarpSmem {
-  unsigned long long fpath[2][FCAP];
-  unsigned char fdep[2][FCAP];
-  double la[LCAP], lb[LCAP], lc[LCAP], ld[LCAP], le[LCAP], lf[LCAP], ls[LCAP];
-  double cc[kMaxModes];
-};
+// K4: near_eval in two stages.
+//  K4a k_near_leaves<FILL>: one thread per (target, element) pair runs the
+//      4-way midpoint subdivision depth-first (child 0 first: the oracle's
+//      recursion order) and counts / writes its accepted leaves as path
+//      codes (2 bits per level, depth in the top 6 bits).
+//  K4b k_near_int<P>: one warp per pair integrates the pair's leaves with the
+//      N_n rule, lanes over (leaf, node) two nodes at a time, and subtracts
+//      the element's far-field point sum.
+constexpr int kMaxPathDepth = 29;
+constexpr int NEAR_WARPS = 8;
+constexpr int kStackCap = 3 * kMaxPathDepth + 4;
+constexpr unsigned long long kPathMask = (1ull << 58) - 1ull;
 
 __device__ __forceinline__ void decode_path(unsigned long long path, int d, double& ax, double& ay,
                                             double& bx, double& by, double& cx, double& cy) {
@@ -301,176 +305,178 @@ __device__ __forceinline__ void decode_path(unsigned long long path, int d, doub
   }
 }
 
-template <int P>
-__device__ void near_flush(NearWarpSmem& W, int nleaf, int lane, const double* __restrict__ nx,
-                           const double* __restrict__ ny, const double* __restrict__ nw, int Ln,
-                           double X0, double Y0, double E1x, double E1y, double E2x, double E2y,
-                           double tx, double ty, double& acc) {
-  const int total = nleaf * Ln;
-  int li = lane / Ln, ni = lane - li * Ln;
-  for (int j = lane; j < total; j += 32) {
-    const double u = nx[ni], v = ny[ni];
-    const double xi = W.la[li] + (u * W.lc[li] + v * W.le[li]);
-    const double eta = W.lb[li] + (u * W.ld[li] + v * W.lf[li]);
-    const double yx = X0 + (xi * E1x + eta * E2x);
-    const double yy = Y0 + (xi * E1y + eta * E2y);
-    const double f = density<P>(W.cc, xi, eta);
-    const double dx = tx - yx, dy = ty - yy;
-    const double r2 = fma(dx, dx, dy * dy);
-    acc = fma(nw[ni] * W.ls[li], f * log(r2), acc);
-    ni += 32;
-    while (ni >= Ln) { ni -= Ln; ++li; }
+// acceptance test of one sub-simplex (same operation order as the oracle's
+// near_rec): rho_d = rho0n 4^{-d/N_n}; rho_d <= 1 accepts.
+__device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double ty, double rd,
+                                            double ax, double ay, double bx, double by, double cx,
+                                            double cy, bool& rle1) {
+  rle1 = false;
+  if (!(rd > 1.0)) {
+    rle1 = true;
+    return true;
+  }
+  const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+  const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
+  double px[3], py[3], dist[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    px[k] = rn_add(E.x0, rn_add(rn_mul(vxs[k], E.e1x), rn_mul(vys[k], E.e2x)));
+    py[k] = rn_add(E.y0, rn_add(rn_mul(vxs[k], E.e1y), rn_mul(vys[k], E.e2y)));
+    dist[k] = rn_dist(tx, ty, px[k], py[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int k1 = (k + 1) % 3;
+    const double len = rn_dist(px[k1], py[k1], px[k], py[k]);
+    if (rn_add(dist[k], dist[k1]) < rn_mul(g, len)) return false;
+  }
+  return true;
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(128)
+    k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
+                  const int32_t* __restrict__ pair_elem, const double2* __restrict__ txy,
+                  const ElemRec* __restrict__ el, const RulesDev* __restrict__ R,
+                  int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                  unsigned long long* __restrict__ leaves, unsigned long long* __restrict__ stats,
+                  int* __restrict__ err) {
+  __shared__ double skd[kMaxNearDepth + 2];
+  for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long rle1 = 0;
+  int maxd = 0;
+  if (p < n_pairs) {
+    const int32_t e = pair_elem[p];
+    const double2 tp = txy[pair_tgt[p]];
+    const ElemRec E = el[e];
+    unsigned long long stack[kStackCap];
+    int sp = 0;
+    stack[sp++] = 0ull;
+    int64_t n = 0, o = FILL ? off[p] : 0;
+    bool bad = false;
+    while (sp > 0) {
+      const unsigned long long code = stack[--sp];
+      const int d = (int)(code >> 58);
+      const unsigned long long path = code & kPathMask;
+      double ax, ay, bx, by, cx, cy;
+      decode_path(path, d, ax, ay, bx, by, cx, cy);
+      bool le1;
+      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1)) {
+        if (FILL) leaves[o++] = code;
+        ++n;
+        rle1 += le1 ? 1ull : 0ull;
+        maxd = max(maxd, d);
+      } else {
+        if (d + 1 > kMaxPathDepth || sp + 4 > kStackCap) {
+          bad = true;
+          break;
+        }
+        const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
+        stack[sp++] = base | 3ull;
+        stack[sp++] = base | 2ull;
+        stack[sp++] = base | 1ull;
+        stack[sp++] = base;
+      }
+    }
+    if (bad) atomicExch(err, 2);
+    if (!FILL) cnt[p] = bad ? 0 : n;
+  }
+  if (!FILL) {
+    for (int o = 16; o > 0; o >>= 1) {
+      rle1 += __shfl_xor_sync(0xffffffffu, rle1, o);
+      maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (rle1) atomicAdd(&stats[1], rle1);
+      atomicMax(&stats[2], (unsigned long long)maxd);
+    }
   }
 }
 
 template <int P>
-__global__ void __launch_bounds__(NEAR_WARPS * 32)
-    k_near(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
-           const double2* __restrict__ txy, const ElemRec* __restrict__ el,
-           const double* __restrict__ coeffs, const double* __restrict__ sx,
-           const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
-           double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ leaves_out,
-           unsigned long long* __restrict__ stats, int* __restrict__ err) {
+__device__ __forceinline__ double near_node(const ShCoef& cc, const double2* __restrict__ ltab,
+                                            double2 a, double2 ba, double2 ca, double sc, double2 nxy, double nw,
+                                            double X0, double Y0, double E1x, double E1y, double E2x,
+                                            double E2y, double tx, double ty) {
+  const double xi = fma(nxy.y, ca.x, fma(nxy.x, ba.x, a.x));
+  const double eta = fma(nxy.y, ca.y, fma(nxy.x, ba.y, a.y));
+  const double yx = fma(eta, E2x, fma(xi, E1x, X0));
+  const double yy = fma(eta, E2y, fma(xi, E1y, Y0));
+  const double f = density<P>(cc, xi, eta);
+  const double dx = tx - yx, dy = ty - yy;
+  return (nw * sc) * f * fast_log_r2<1>(ltab, fma(dx, dx, dy * dy));
+}
+
+template <int P>
+__global__ void __launch_bounds__(NEAR_WARPS * 32, 3)
+    k_near_int(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
+               const double2* __restrict__ txy, const ElemRec* __restrict__ el,
+               const double* __restrict__ coeffs, const int64_t* __restrict__ loff,
+               const unsigned long long* __restrict__ leaves, const double* __restrict__ sx,
+               const double* __restrict__ sy, const double* __restrict__ sq,
+               const RulesDev* __restrict__ R, double* __restrict__ corr, double* __restrict__ sub_out) {
   constexpr int M = (P + 1) * (P + 2) / 2;
-  __shared__ NearWarpSmem Wsm[NEAR_WARPS];
-  __shared__ double snx[kMaxNearRule], sny[kMaxNearRule], snw[kMaxNearRule], skd[kMaxNearDepth + 2];
+  __shared__ double scc[NEAR_WARPS][M];
+  __shared__ double2 sga[NEAR_WARPS][32], sgb[NEAR_WARPS][32], sgc[NEAR_WARPS][32];
+  __shared__ double sgs[NEAR_WARPS][32];
+  __shared__ double2 snxy[kMaxNearRule];
+  __shared__ double snw[kMaxNearRule];
+  __shared__ double2 sltab[kLogEntries];
   const int Ln = R->len_n, len_q = R->len_q;
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
   for (int i = threadIdx.x; i < Ln; i += blockDim.x) {
-    snx[i] = R->near_x[i];
-    sny[i] = R->near_y[i];
+    snxy[i] = make_double2(R->near_x[i], R->near_y[i]);
     snw[i] = R->near_w[i];
   }
-  for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  NearWarpSmem& W = Wsm[wid];
-  const unsigned lt_mask = (1u << lane) - 1u;
-  unsigned long long my_leaves = 0, my_rle1 = 0;
-  int my_maxd = 0;
-  for (int64_t p = (int64_t)blockIdx.x * NEAR_WARPS + wid; p < n_pairs;
-       p += (int64_t)gridDim.x * NEAR_WARPS) {
+  double* cc = scc[wid];
+  for (int64_t p = (int64_t)blockIdx.x * NEAR_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * NEAR_WARPS) {
     const int32_t t = pair_tgt[p], e = pair_elem[p];
     const double2 tp = txy[t];
     const double tx = tp.x, ty = tp.y;
     const ElemRec& Er = el[e];
     const double X0 = Er.x0, Y0 = Er.y0, E1x = Er.e1x, E1y = Er.e1y, E2x = Er.e2x, E2y = Er.e2y;
-    const double det = Er.det, rho0n = Er.rho0n;
-    for (int j = lane; j < M; j += 32) W.cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
-    if (lane == 0) {
-      W.fpath[0][0] = 0ull;
-      W.fdep[0][0] = 0;
-    }
-    __syncwarp();
-    int cur = 0, fcnt = 1, nleaf = 0;
+    const double det = Er.det;
+    for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    const int64_t l0 = loff[p], nl = loff[p + 1] - l0;
     double acc = 0.0;
-    long long pair_leaves = 0;
-    bool bad = false;
-    while (fcnt > 0 && !bad) {
-      int ncnt = 0;
-      for (int base = 0; base < fcnt; base += 32) {
-        const int i = base + lane;
-        const bool act = i < fcnt;
-        bool accept = false;
-        unsigned long long path = 0;
-        int d = 0;
-        double ax = 0, ay = 0, bx = 0, by = 0, cx = 0, cy = 0;
-        if (act) {
-          path = W.fpath[cur][i];
-          d = W.fdep[cur][i];
-          decode_path(path, d, ax, ay, bx, by, cx, cy);
-          const double rd = rn_mul(rho0n, skd[d]);
-          if (!(rd > 1.0)) {
-            accept = true;
-            ++my_rle1;
-          } else {
-            const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
-            const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
-            double px[3], py[3], dist[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              px[k] = rn_add(X0, rn_add(rn_mul(vxs[k], E1x), rn_mul(vys[k], E2x)));
-              py[k] = rn_add(Y0, rn_add(rn_mul(vxs[k], E1y), rn_mul(vys[k], E2y)));
-              dist[k] = rn_dist(tx, ty, px[k], py[k]);
-            }
-            bool nearp = false;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-              const int k1 = (k + 1) % 3;
-              const double len = rn_dist(px[k1], py[k1], px[k], py[k]);
-              if (rn_add(dist[k], dist[k1]) < rn_mul(g, len)) nearp = true;
-            }
-            accept = !nearp;
-          }
-        }
-        const unsigned am = __ballot_sync(0xffffffffu, act && accept);
-        const unsigned rm = __ballot_sync(0xffffffffu, act && !accept);
-        const int na = __popc(am);
-        if (nleaf + na > LCAP) {
-          __syncwarp();
-          near_flush<P>(W, nleaf, lane, snx, sny, snw, Ln, X0, Y0, E1x, E1y, E2x, E2y, tx, ty, acc);
-          __syncwarp();
-          nleaf = 0;
-        }
-        if (act && accept) {
-          const int slot = nleaf + __popc(am & lt_mask);
-          W.la[slot] = ax;
-          W.lb[slot] = ay;
-          W.lc[slot] = bx - ax;
-          W.ld[slot] = by - ay;
-          W.le[slot] = cx - ax;
-          W.lf[slot] = cy - ay;
-          W.ls[slot] = det * ldexp(1.0, -2 * d) * kInv4Pi;
-          if (d > my_maxd) my_maxd = d;
-        }
-        nleaf += na;
-        pair_leaves += na;
-        if (act && !accept) {
-          const int slot = ncnt + 4 * __popc(rm & lt_mask);
-          if (d + 1 > kMaxPathDepth || slot + 3 >= FCAP) {
-            bad = true;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              W.fpath[cur ^ 1][slot + c] = (path << 2) | (unsigned long long)c;
-              W.fdep[cur ^ 1][slot + c] = (unsigned char)(d + 1);
-            }
-          }
-        }
-        ncnt += 4 * __popc(rm);
-        bad = __any_sync(0xffffffffu, bad);
+    for (int64_t lb = 0; lb < nl; lb += 32) {
+      const int nb = (int)min((int64_t)32, nl - lb);
+      __syncwarp();
+      if (lane < nb) {
+        const unsigned long long code = leaves[l0 + lb + lane];
+        const int d = (int)(code >> 58);
+        double ax, ay, bx, by, cx, cy;
+        decode_path(code & kPathMask, d, ax, ay, bx, by, cx, cy);
+        sga[wid][lane] = make_double2(ax, ay);
+        sgb[wid][lane] = make_double2(bx - ax, by - ay);
+        sgc[wid][lane] = make_double2(cx - ax, cy - ay);
+        sgs[wid][lane] = det * ldexp(1.0, -2 * d) * kInv4Pi;
       }
       __syncwarp();
-      cur ^= 1;
-      fcnt = ncnt;
+      const int total = nb * Ln;
+      // node j = (li, ni), lanes strided by 32
+      int li = lane / Ln, ni = lane - li * Ln;
+      for (int j = lane; j < total; j += 32) {
+        acc += near_node<P>(ShCoef(cc), sltab, sga[wid][li], sgb[wid][li], sgc[wid][li], sgs[wid][li], snxy[ni],
+                            snw[ni], X0, Y0, E1x, E1y, E2x, E2y, tx, ty);
+        ni += 32;
+        while (ni >= Ln) { ni -= Ln; ++li; }
+      }
     }
-    if (bad) {
-      if (lane == 0) atomicExch(err, 2);
-      nleaf = 0;
-    }
-    __syncwarp();
-    near_flush<P>(W, nleaf, lane, snx, sny, snw, Ln, X0, Y0, E1x, E1y, E2x, E2y, tx, ty, acc);
     const double val = warp_sum(acc);
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab);
     if (lane == 0) {
-      corr[p] = val - sub;
       if (sub_out) {
         corr[p] = val;
         sub_out[p] = sub;
+      } else {
+        corr[p] = val - sub;
       }
-      if (leaves_out) leaves_out[p] = pair_leaves;
     }
-    my_leaves += (lane == 0) ? (unsigned long long)pair_leaves : 0ull;
-    __syncwarp();
-  }
-  // my_rle1 counted per lane for accepted items; sum over the warp
-  unsigned long long r = my_rle1;
-  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  int md = my_maxd;
-  for (int o = 16; o > 0; o >>= 1) md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
-  if (lane == 0) {
-    if (my_leaves) atomicAdd(&stats[0], my_leaves);
-    if (r) atomicAdd(&stats[1], r);
-    atomicMax((unsigned long long*)&stats[2], (unsigned long long)md);
   }
 }
 
@@ -520,7 +526,7 @@ __device__ __forceinline__ double self_bnd(const SelfGeom& G, int i) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(SELF_WARPS * 32)
+__global__ void __launch_bounds__(SELF_WARPS * 32, 6)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
            const double2* __restrict__ txy, const ElemRec* __restrict__ el,
            const double* __restrict__ coeffs, const double* __restrict__ sx,
@@ -530,6 +536,8 @@ __global__ void __launch_bounds__(SELF_WARPS * 32)
   constexpr int M = (P + 1) * (P + 2) / 2;
   __shared__ double scc[SELF_WARPS][kMaxModes];
   __shared__ double sglx[kMaxGL], sglw[kMaxGL], sgr[kMaxGGQ], sgw[kMaxGGQ], sglr[kMaxGGQ];
+  __shared__ double2 sltab[kLogEntries];
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
   const int NL = R->n_l, NG = R->n_g1, len_q = R->len_q;
   for (int i = threadIdx.x; i < NL; i += blockDim.x) {
     sglx[i] = R->gl_x[i];
@@ -563,20 +571,25 @@ __global__ void __launch_bounds__(SELF_WARPS * 32)
     rn_locate(Er, tx, ty, txi, teta);
     for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
     __syncwarp();
-    const double vx[3] = {Er.x0, Er.x1, Er.x2}, vy[3] = {Er.y0, Er.y1, Er.y2};
-    const double rx[3] = {0.0, 1.0, 0.0}, ry[3] = {0.0, 0.0, 1.0};
     double acc = 0.0;
     long long npan_item = 0;
+#pragma unroll 1
     for (int k = 0; k < 3; ++k) {
-      const int k1 = (k + 1) % 3;
+      // side (A, B) = (v_k, v_{k+1}); reference corners (0,0), (1,0), (0,1)
+      const double Ax = k == 0 ? Er.x0 : (k == 1 ? Er.x1 : Er.x2);
+      const double Ay = k == 0 ? Er.y0 : (k == 1 ? Er.y1 : Er.y2);
+      const double Bx = k == 0 ? Er.x1 : (k == 1 ? Er.x2 : Er.x0);
+      const double By = k == 0 ? Er.y1 : (k == 1 ? Er.y2 : Er.y0);
       SelfGeom G;
-      self_geom(tx, ty, vx[k], vy[k], vx[k1], vy[k1], G);
+      self_geom(tx, ty, Ax, Ay, Bx, By, G);
       if (G.degenerate) {
         ++my_degen;  // identical in every lane; counted once below
         continue;
       }
-      const double Arx = rx[k], Ary = ry[k], BRx = rx[k1] - rx[k], BRy = ry[k1] - ry[k];
+      const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
+      const double BRx = (k == 0 ? 1.0 : 0.0) - Arx, BRy = (k == 1 ? 1.0 : 0.0) - Ary;
       const int nodes = G.npan * NL;
+      const double invL = 1.0 / G.L;
       for (int j = lane; j < nodes; j += 32) {
         const int pi = j / NL, gq = j - pi * NL;
         const double s0 = self_bnd(G, pi), s1 = self_bnd(G, pi + 1);
@@ -584,15 +597,15 @@ __global__ void __launch_bounds__(SELF_WARPS * 32)
         const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
         const double s = fma(half, sglx[gq], mid);
         const double ws = half * sglw[gq];
-        const double sl = s / G.L;
+        const double sl = s * invL;
         const double px = fma(sl, G.ABx, G.Ax), py = fma(sl, G.ABy, G.Ay);
         const double ddx = px - tx, ddy = py - ty;
-        const double lr0 = 0.5 * log(fma(ddx, ddx, ddy * ddy));
+        const double lr0 = 0.5 * fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
         const double grx = fma(sl, BRx, Arx) - txi, gry = fma(sl, BRy, Ary) - teta;
         double inner = 0.0;
         for (int q = 0; q < NG; ++q) {
           const double rj = sgr[q];
-          const double f = density<P>(cc, fma(rj, grx, txi), fma(rj, gry, teta));
+          const double f = density<P>(ShCoef(cc), fma(rj, grx, txi), fma(rj, gry, teta));
           inner = fma(sgw[q] * (lr0 + sglr[q]), f, inner);
         }
         acc = fma(ws * G.h, inner, acc);
@@ -601,7 +614,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32)
         if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
     const double val = warp_sum(acc) * kInv2Pi;
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab);
     if (lane == 0) {
       corr[it] = sub_out ? val : val - sub;
       if (sub_out) sub_out[it] = sub;
@@ -717,7 +730,8 @@ struct vp_ctx {
   DevBuf d_sx, d_sy, d_sq;
   // per-evaluation scratch
   DevBuf d_txy, d_u, d_ufar, d_part, d_self, d_cnt, d_off, d_ids, d_ptgt, d_corr, d_corr_self,
-      d_selfref, d_stats, d_err, d_tmp, d_sub, d_leaves, d_pelem;
+      d_selfref, d_stats, d_err, d_tmp, d_sub, d_leaves, d_pelem, d_lcnt, d_loff, d_leafcodes;
+  int64_t n_leaves_last = 0;
   cudaEvent_t ev[8] = {};
   int last_launches = 0;
 };
@@ -873,26 +887,6 @@ int build_elements(vp_ctx* c) {
   return 0;
 }
 
-template <int P>
-void launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
-                 double* corr, double* sub, int64_t* leaves) {
-  const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 64);
-  k_near<P><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
-      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, leaves,
-      c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
-}
-
-template <int P>
-void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
-                 double* corr, double* sub, int64_t* panels) {
-  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
-  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
-      n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
-      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
-      c->d_stats.as<unsigned long long>());
-}
-
 #define VP_DISPATCH_P(p, F, ...)      \
   switch (p) {                        \
     case 0: F<0>(__VA_ARGS__); break;   \
@@ -910,6 +904,57 @@ void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem
     case 12: F<12>(__VA_ARGS__); break; \
     default: break;                     \
   }
+
+template <int P>
+void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
+                     double* corr, double* sub) {
+  const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 32);
+  k_near_int<P><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
+      c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
+      c->d_rules.as<RulesDev>(), corr, sub);
+}
+
+int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
+                double* corr, double* sub, int64_t* leaves_host) {
+  CUDA_TRY(c, c->d_lcnt.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_loff.ensure(sizeof(int64_t) * (n + 1)));
+  k_near_leaves<false><<<nblk(n, 128), 128, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), nullptr,
+      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+  CUDA_TRY(c, cudaMemsetAsync(c->d_lcnt.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
+  size_t tmpb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1,
+                                c->stream);
+  int64_t nleaves = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&nleaves, c->d_loff.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, c->d_leafcodes.ensure(sizeof(unsigned long long) * (nleaves + 1)));
+  k_near_leaves<true><<<nblk(n, 128), 128, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
+      c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+  VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub);
+  CUDA_TRY(c, cudaGetLastError());
+  c->n_leaves_last = nleaves;
+  c->last_launches += 5;
+  if (leaves_host)
+    CUDA_TRY(c, cudaMemcpyAsync(leaves_host, c->d_lcnt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  return 0;
+}
+
+template <int P>
+void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
+                 double* corr, double* sub, int64_t* panels) {
+  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
+  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
+      n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
+      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
+      c->d_stats.as<unsigned long long>());
+}
+
 
 int ensure_ready(vp_ctx* c, bool need_density) {
   if (!c) return 1;
@@ -938,11 +983,12 @@ int compute_sources(vp_ctx* c) {
 int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar) {
   const int64_t S = c->n_tri * c->rules.len_q;
   const int64_t tblocks = nblk(T, FAR_THREADS * FAR_R);
-  // split sources so the grid covers >= 4 waves of the SMs
-  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4LL * c->sm_count + tblocks - 1) / tblocks));
-  int64_t chunk = (S + nsplit - 1) / nsplit;
+  // The source chunking depends on S only, never on T: every target's far
+  // sum is the same fixed-order sum of chunk partials however the targets
+  // are batched or sharded (bitwise shard invariance).
+  int64_t chunk = std::max<int64_t>(4096, (S + 63) / 64);
   chunk = (chunk + FAR_TILE - 1) / FAR_TILE * FAR_TILE;
-  nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
+  const int nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
   CUDA_TRY(c, c->d_part.ensure(sizeof(double) * T * nsplit));
   dim3 grid((unsigned)tblocks, (unsigned)nsplit);
   k_far<<<grid, FAR_THREADS, 0, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
@@ -1005,9 +1051,9 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * (n_ids + 1)));
   if (n_ids > 0) {
     k_pair_tgt<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), c->d_ptgt.as<int32_t>());
-    VP_DISPATCH_P(c->p, launch_near, c, n_ids, c->d_ptgt.as<int32_t>(), c->d_ids.as<int32_t>(), txy,
-                  c->d_corr.as<double>(), nullptr, nullptr);
-    c->last_launches += 2;
+    c->last_launches += 1;
+    if (int rc = launch_near(c, n_ids, c->d_ptgt.as<int32_t>(), c->d_ids.as<int32_t>(), txy,
+                             c->d_corr.as<double>(), nullptr, nullptr)) return rc;
   }
   CUDA_TRY(c, cudaEventRecord(ev[3], c->stream));
   CUDA_TRY(c, c->d_corr_self.ensure(sizeof(double) * (T + 1)));
@@ -1032,7 +1078,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     std::memset(st, 0, sizeof(*st));
     st->n_targets = T;
     st->n_near_pairs = n_ids;
-    st->n_leaves = (int64_t)hs[0];
+    st->n_leaves = n_ids > 0 ? c->n_leaves_last : 0;
     st->n_rho_le1 = (int64_t)hs[1];
     st->max_depth = (int32_t)hs[2];
     st->n_panels = (int64_t)hs[3];
@@ -1091,7 +1137,10 @@ int vp_create(int device, vp_ctx** out) {
   double cn[kMaxModes];
   for (int n2 = 0; n2 <= kMaxPdev; ++n2)
     for (int m = 0; m <= n2; ++m) cn[koorn_index(m, n2)] = std::sqrt((double)((2 * m + 1) * (2 * n2 + 2)));
-  if (cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess) {
+  double2 lt[kLogEntries];
+  log_table_fill(lt);
+  if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess) {
     vp_destroy(c);
     return 3;
   }
@@ -1359,8 +1408,9 @@ static int pairs_common(vp_ctx* c, int64_t n, const double* txy, const int32_t* 
     VP_DISPATCH_P(c->p, launch_self, c, n, c->d_ptgt.as<int32_t>(), c->d_pelem.as<int32_t>(),
                   c->d_txy.as<double2>(), c->d_corr.as<double>(), c->d_sub.as<double>(), c->d_leaves.as<int64_t>());
   } else {
-    VP_DISPATCH_P(c->p, launch_near, c, n, c->d_ptgt.as<int32_t>(), c->d_pelem.as<int32_t>(),
-                  c->d_txy.as<double2>(), c->d_corr.as<double>(), c->d_sub.as<double>(), c->d_leaves.as<int64_t>());
+    if (int rc = launch_near(c, n, c->d_ptgt.as<int32_t>(), c->d_pelem.as<int32_t>(), c->d_txy.as<double2>(),
+                             c->d_corr.as<double>(), c->d_sub.as<double>(), nullptr)) return rc;
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_leaves.p, c->d_lcnt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
   }
   CUDA_TRY(c, cudaGetLastError());
   int herr = 0;

@@ -85,40 +85,118 @@ __host__ __device__ constexpr double kc_jc(int m, int k) {
 }
 
 // f(x, y) = sum_j cc_j K_j(x, y) where cc_j already includes the
-// normalisation c_mn (pre-scaled per element).  ~4 FP64 ops per mode.
-template <int P>
-__device__ __forceinline__ double density(const double* __restrict__ cc, double x, double y) {
+// normalisation c_mn (pre-scaled per element).  Template recursion over
+// (m, k) makes every recurrence coefficient a compile-time constant (no
+// runtime divisions); ~4 FP64 ops per mode.
+// Coefficient accessor for shared memory: an `ld.shared` in volatile asm is
+// re-issued at every use (a broadcast LDS, one wavefront), so the
+// coefficients are never hoisted into (and spilled from) registers.
+struct ShCoef {
+  unsigned base;
+  __device__ __forceinline__ explicit ShCoef(const double* p)
+      : base((unsigned)__cvta_generic_to_shared(p)) {}
+  __device__ __forceinline__ double operator[](int i) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (unsigned)i));
+    return v;
+  }
+};
+
+template <int P, int m, int k, class CC>
+__device__ __forceinline__ void jacobi_tail(const CC& cc, double t, double& p0, double& p1, double& s) {
+  if constexpr (m + k + 1 <= P) {
+    constexpr double ja = kc_ja(m, k), jb = kc_jb(m, k), jc = kc_jc(m, k);
+    const double al = fma(ja, t, jb);
+    const double p2 = fma(al, p1, -jc * p0);
+    s = fma(cc[koorn_index(m, m + k + 1)], p2, s);
+    p0 = p1;
+    p1 = p2;
+    jacobi_tail<P, m, k + 1, CC>(cc, t, p0, p1, s);
+  }
+}
+
+template <int P, int m, class CC>
+__device__ __forceinline__ void koorn_modes(const CC& cc, double t, double u, double v2, double Lm,
+                                            double Lprev, double& f) {
+  if constexpr (m <= P) {
+    double s = cc[koorn_index(m, m)];
+    if constexpr (m + 1 <= P) {
+      constexpr double a = 2 * m + 1;
+      constexpr double j1a = 0.5 * (a + 2.0), j1b = 0.5 * a;
+      double p0 = 1.0;
+      double p1 = fma(j1a, t, j1b);
+      s = fma(cc[koorn_index(m, m + 1)], p1, s);
+      jacobi_tail<P, m, 1, CC>(cc, t, p0, p1, s);
+    }
+    f = fma(s, Lm, f);
+    if constexpr (m < P) {
+      double Ln;
+      if constexpr (m == 0) {
+        Ln = u;
+      } else {
+        constexpr double la = kc_la(m), lb = kc_lb(m);
+        Ln = fma(la * u, Lm, -lb * v2 * Lprev);
+      }
+      koorn_modes<P, m + 1, CC>(cc, t, u, v2, Ln, Lm, f);
+    }
+  }
+}
+
+template <int P, class CC>
+__device__ __forceinline__ double density(const CC& cc, double x, double y) {
   const double v = 1.0 - x;
   const double u = fma(2.0, y, -v);
   const double v2 = v * v;
   const double t = fma(2.0, x, -1.0);
-  double Lm = 1.0, Lprev = 0.0, f = 0.0;
-#pragma unroll
-  for (int m = 0; m <= P; ++m) {
-    double s = cc[koorn_index(m, m)];
-    if (m + 1 <= P) {
-      const double a = 2 * m + 1;
-      double p0 = 1.0;
-      double p1 = fma(0.5 * (a + 2.0), t, 0.5 * a);
-      s = fma(cc[koorn_index(m, m + 1)], p1, s);
-#pragma unroll
-      for (int k = 1; m + k + 1 <= P; ++k) {
-        const double al = fma(kc_ja(m, k), t, kc_jb(m, k));
-        const double p2 = fma(al, p1, -kc_jc(m, k) * p0);
-        s = fma(cc[koorn_index(m, m + k + 1)], p2, s);
-        p0 = p1;
-        p1 = p2;
-      }
-    }
-    f = fma(s, Lm, f);
-    if (m < P) {
-      const double Ln = (m == 0) ? u : fma(kc_la(m) * u, Lm, -kc_lb(m) * v2 * Lprev);
-      Lprev = Lm;
-      Lm = Ln;
-    }
-  }
+  double f = 0.0;
+  koorn_modes<P, 0, CC>(cc, t, u, v2, 1.0, 0.0, f);
   return f;
 }
+
+// ---------------------------------------------------------------------------
+// fp64 log of x = r^2 > 0 with 13 FP64 operations (vs ~30 for libdevice):
+//   x = 2^e m, m in [1,2); k = top 8 mantissa bits; r_k ~ 1/(1 + (k+1/2)/256)
+//   log x = e ln2 - log r_k + log(1 + t),  t = m r_k - 1 (one FMA), |t| <= 2^-9
+//   log(1+t) by a degree-5 Taylor polynomial (truncation <= 1e-17).
+// The table {r_k, -log r_k} lives in shared memory, replicated 8x so that
+// the 8 lanes of a quarter-warp hit 8 different bank groups (conflict-free
+// 128-bit loads).  x == 0 (coincident pair) returns 0.
+constexpr int kLogBits = 8;
+constexpr int kLogEntries = 1 << kLogBits;
+constexpr int kLogCopies = 8;
+
+struct LogTab {
+  double2 e[kLogEntries * kLogCopies];  // entry k, copy c at k*8 + c
+};
+
+inline void log_table_fill(double2* host /* kLogEntries */) {
+  for (int k = 0; k < kLogEntries; ++k) {
+    const long double mk = 1.0L + ((long double)k + 0.5L) / (long double)kLogEntries;
+    const double r = (double)(1.0L / mk);
+    host[k].x = r;
+    host[k].y = (double)(-log1pl((long double)r - 1.0L));
+  }
+}
+
+#ifdef __CUDACC__
+// base: this lane's copy (tab + (lane & 7) with STRIDE = kLogCopies), or an
+// unreplicated table with STRIDE = 1
+template <int STRIDE>
+__device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const double2 tb = base[((hi >> (20 - kLogBits)) & (kLogEntries - 1)) * STRIDE];
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double ed = __hiloint2double(0x43380000, hi >> 20) - 6755399441056767.0;  // e = biased - 1023
+  const double t = fma(m, tb.x, -1.0);
+  double i = fma(t, 0.2, -0.25);
+  i = fma(t, i, 0.33333333333333333);
+  i = fma(t, i, -0.5);
+  i = fma(t, i, 1.0);
+  const double p = fma(t, i, tb.y);
+  const double lg = fma(ed, 0.69314718055994530942, p);
+  return hi >= 0x00100000 ? lg : 0.0;
+}
+#endif
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
