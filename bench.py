@@ -34,7 +34,13 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-FAR_FLOP_PER_PAIR = 51  # algorithmic flops per far pair
+# Algorithmic work of one far pair as formulated on B200:
+# dx, dy (2 DADD), r^2 (DMUL + DFMA), log r^2 (1 DADD + 8 DFMA), accumulate
+# (1 DFMA) = 13 FP64 operations = 9 FMA (2 flops) + 4 add/mul (1 flop) = 22 flops.
+FAR_FLOP_PER_PAIR = 22
+# SURVEY.md §8(d)'s frozen figure counted the libdevice log (51 flops/pair);
+# reported beside the roofline for comparison.
+SURVEY_FAR_FLOP_PER_PAIR = 51
 
 
 def parse():
@@ -297,7 +303,8 @@ def main():
         out = {
             "metric": "potential targets/sec (fp64)", "value": value, "unit": "targets/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "step_ms_min": min(ms_steps), "step_ms_max": max(ms_steps),
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, SURVEY.md §8(d)); L2 flushed between timed steps",
             "config": {"workload": f"config{pr.config}", "n_tri": pr.n_tri, "p": pr.p, "q": pr.q,
@@ -306,7 +313,8 @@ def main():
                        "l2": "flushed (256 MB write) between timed steps",
                        "parallelism": f"weak x{world} (targets sharded, mesh+density replicated)"},
             "near_pair_integrals_per_s": world * n_pairs / (pair_ms * 1e-3),
-            "split_ms": {"list": float(np.mean([s["t_list_ms"] for s in stats])),
+            "split_ms": {"lib_device_total": float(np.mean([s["t_total_ms"] for s in stats])),
+                         "list": float(np.mean([s["t_list_ms"] for s in stats])),
                          "sources": float(np.mean([s["t_sources_ms"] for s in stats])),
                          "far": far_ms,
                          "near": float(np.mean([s["t_near_ms"] for s in stats])),
@@ -315,7 +323,11 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "flop_per_launch": far_flop, "flop_per_pair": FAR_FLOP_PER_PAIR,
-                         "traffic": prof.get("dram_bytes_per_launch")},
+                         "pairs_per_s": T * S / (far_ms * 1e-3),
+                         "survey_flop_per_pair": SURVEY_FAR_FLOP_PER_PAIR,
+                         "survey_equiv_tflops": SURVEY_FAR_FLOP_PER_PAIR * T * S / (far_ms * 1e-3) / 1e12,
+                         "traffic": prof.get("dram_bytes_per_launch"),
+                         "traffic_source": prof.get("source")},
             "gpu_launches": int(sum(s["gpu_launches"] for s in stats)),
             "clocks": clocks,
             "e2e": e2e,

@@ -203,15 +203,22 @@ constexpr int FAR_TILE = 256;
 
 __device__ double2 g_logtab[kLogEntries];  // {r_k, -log r_k}, filled at vp_create
 
+// The replicated log table must start at a shared offset aligned to its
+// size (32 KB) so entry offsets can be OR-ed with the lane's copy address.
+template <bool ZERO_CHECK>
 __global__ void __launch_bounds__(FAR_THREADS, 2)
     k_far(int64_t T, const double2* __restrict__ txy, int64_t S, const double* __restrict__ sx,
           const double* __restrict__ sy, const double* __restrict__ sq, int64_t chunk,
-          double* __restrict__ part) {
-  __shared__ LogTab tab;
-  __shared__ double2 sxy[FAR_TILE];
-  __shared__ double ssq[FAR_TILE];
-  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += FAR_THREADS) tab.e[i] = g_logtab[i / kLogCopies];
-  const double2* lbase = tab.e + (threadIdx.x & (kLogCopies - 1));
+          double* __restrict__ part, unsigned c3ff) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  // layout: [pad to 32 KB boundary][log table 32 KB][sources]
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(fsm);
+  const unsigned tab_off = ((sbase + 32767u) & ~32767u) - sbase;
+  double2* tab = (double2*)(fsm + tab_off);
+  double2* sxy = (double2*)(fsm + tab_off + sizeof(LogTab));
+  double* ssq = (double*)(sxy + FAR_TILE);
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += FAR_THREADS) tab[i] = g_logtab[i / kLogCopies];
+  const unsigned lane_tab = sbase + tab_off + 16u * (threadIdx.x & (kLogCopies - 1));
   const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
   double tx[FAR_R], ty[FAR_R], acc[FAR_R];
 #pragma unroll
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(FAR_THREADS, 2)
       for (int r = 0; r < FAR_R; ++r) {
         const double dx = tx[r] - ps.x, dy = ty[r] - ps.y;
         const double r2 = fma(dx, dx, dy * dy);
-        acc[r] = fma(q, fast_log_r2<kLogCopies>(lbase, r2), acc[r]);
+        acc[r] = fma(q, far_log_r2<ZERO_CHECK>(lane_tab, c3ff, r2), acc[r]);
       }
     }
   }
@@ -250,6 +257,8 @@ __global__ void __launch_bounds__(FAR_THREADS, 2)
     if (t < T) part[(int64_t)blockIdx.y * T + t] = acc[r];
   }
 }
+
+constexpr size_t kFarSmem = 32768 + sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeof(double));
 
 __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ part,
                              double* __restrict__ u) {
@@ -980,7 +989,7 @@ int compute_sources(vp_ctx* c) {
   return 0;
 }
 
-int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar) {
+int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check) {
   const int64_t S = c->n_tri * c->rules.len_q;
   const int64_t tblocks = nblk(T, FAR_THREADS * FAR_R);
   // The source chunking depends on S only, never on T: every target's far
@@ -991,8 +1000,14 @@ int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar) {
   const int nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
   CUDA_TRY(c, c->d_part.ensure(sizeof(double) * T * nsplit));
   dim3 grid((unsigned)tblocks, (unsigned)nsplit);
-  k_far<<<grid, FAR_THREADS, 0, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                             c->d_sq.as<double>(), chunk, c->d_part.as<double>());
+  if (zero_check)
+    k_far<true><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                                          c->d_sq.as<double>(), chunk, c->d_part.as<double>(),
+                                                          0x3ff00000u);
+  else
+    k_far<false><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                                           c->d_sq.as<double>(), chunk, c->d_part.as<double>(),
+                                                           0x3ff00000u);
   k_far_reduce<<<nblk(T, 256), 256, 0, c->stream>>>(T, nsplit, c->d_part.as<double>(), ufar);
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 2;
@@ -1045,7 +1060,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   if (int rc = compute_sources(c)) return rc;
   CUDA_TRY(c, cudaEventRecord(ev[6], c->stream));
   CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * (T + 1)));
-  if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>())) return rc;
+  if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false)) return rc;
   CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
   CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * (n_ids + 1)));
   CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * (n_ids + 1)));
@@ -1137,6 +1152,11 @@ int vp_create(int device, vp_ctx** out) {
   double cn[kMaxModes];
   for (int n2 = 0; n2 <= kMaxPdev; ++n2)
     for (int m = 0; m <= n2; ++m) cn[koorn_index(m, n2)] = std::sqrt((double)((2 * m + 1) * (2 * n2 + 2)));
+  if (cudaFuncSetAttribute(k_far<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_far<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess) {
+    vp_destroy(c);
+    return 3;
+  }
   double2 lt[kLogEntries];
   log_table_fill(lt);
   if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
@@ -1363,7 +1383,7 @@ int vp_far_field(vp_ctx* c, int64_t n_tgt, const double* txy, double* u_far) {
   CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * n_tgt));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n_tgt, cudaMemcpyHostToDevice, c->stream));
   if (int rc = compute_sources(c)) return rc;
-  if (int rc = far_sum(c, n_tgt, c->d_txy.as<double2>(), c->d_ufar.as<double>())) return rc;
+  if (int rc = far_sum(c, n_tgt, c->d_txy.as<double2>(), c->d_ufar.as<double>(), true)) return rc;
   CUDA_TRY(c, cudaMemcpyAsync(u_far, c->d_ufar.p, sizeof(double) * n_tgt, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return 0;

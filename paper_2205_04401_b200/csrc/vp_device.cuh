@@ -196,6 +196,37 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
   const double lg = fma(ed, 0.69314718055994530942, p);
   return hi >= 0x00100000 ? lg : 0.0;
 }
+
+// Far-kernel variant of fast_log_r2 with fewer integer operations:
+//   * `lane_tab` is the byte address (shared window) of this lane's copy of
+//     the replicated table; the entry offset (k*128) is OR-ed in with one LOP3;
+//   * the mantissa m is built with one LOP3 using `c3ff` = 0x3ff00000 held in
+//     a register;
+//   * ZERO_CHECK = false skips the r^2 == 0 test.  That is exact for the
+//     evaluation path: a target can only coincide with an interior node of
+//     its own element S(t), whose point sum is subtracted again with the same
+//     function (subtract-and-add), so the finite value
+//     returned for r^2 == 0 cancels.
+template <bool ZERO_CHECK>
+__device__ __forceinline__ double far_log_r2(unsigned lane_tab, unsigned c3ff, double x) {
+  const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+  unsigned off, mhi;
+  asm("lop3.b32 %0, %1, 0x7f80, %2, 0xEA;" : "=r"(off) : "r"(hi >> 5), "r"(lane_tab));
+  asm("lop3.b32 %0, %1, 0x000fffff, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(c3ff));
+  double rk, lk;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(rk), "=d"(lk) : "r"(off));
+  const double m = __hiloint2double((int)mhi, (int)lo);
+  const double ed = __hiloint2double(0x43380000, (int)(hi >> 20)) - 6755399441056767.0;
+  const double t = fma(m, rk, -1.0);
+  double i = fma(t, 0.2, -0.25);
+  i = fma(t, i, 0.33333333333333333);
+  i = fma(t, i, -0.5);
+  i = fma(t, i, 1.0);
+  const double p = fma(t, i, lk);
+  const double lg = fma(ed, 0.69314718055994530942, p);
+  if constexpr (ZERO_CHECK) return hi >= 0x00100000u ? lg : 0.0;
+  return lg;
+}
 #endif
 
 __device__ __forceinline__ double warp_sum(double v) {
