@@ -35,9 +35,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 # Algorithmic work of one far pair as formulated on B200:
-# dx, dy (2 DADD), r^2 (DMUL + DFMA), log r^2 (1 DADD + 8 DFMA), accumulate
-# (1 DFMA) = 13 FP64 operations = 9 FMA (2 flops) + 4 add/mul (1 flop) = 22 flops.
-FAR_FLOP_PER_PAIR = 22
+# dx, dy (2 DADD), r^2 (DMUL + DFMA), log r^2 (6 DFMA: t, 4-term polynomial,
+# exponent), accumulate (1 DFMA) = 11 FP64 operations = 8 FMA (2 flops) +
+# 3 add/mul (1 flop) = 19 flops.  (The exponent's int->double conversion runs
+# on the XU pipe.)
+FAR_FLOP_PER_PAIR = 19
 # SURVEY.md §8(d)'s frozen figure counted the libdevice log (51 flops/pair);
 # reported beside the roofline for comparison.
 SURVEY_FAR_FLOP_PER_PAIR = 51

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvp_b200.so")
+# VP_B200_LIB overrides the library path (development builds / variant sweeps)
+LIB_PATH = os.environ.get("VP_B200_LIB", os.path.join(_HERE, "libvp_b200.so"))
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_int32_p = ctypes.POINTER(ctypes.c_int32)

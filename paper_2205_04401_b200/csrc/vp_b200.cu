@@ -197,28 +197,29 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 // Sources are staged through shared memory and broadcast to the block's
 // targets; each thread keeps FAR_R targets in registers.  The source range
 // is split over gridDim.y; partials are reduced in fixed order.
+#ifndef VP_FAR_R
+#define VP_FAR_R 8
+#endif
+#ifndef VP_FAR_MINB
+#define VP_FAR_MINB 2
+#endif
 constexpr int FAR_THREADS = 256;
-constexpr int FAR_R = 8;
-constexpr int FAR_TILE = 256;
+constexpr int FAR_R = VP_FAR_R;      // targets per thread (register tile)
+constexpr int FAR_TILE = 256;        // sources per shared-memory tile
 
 __device__ double2 g_logtab[kLogEntries];  // {r_k, -log r_k}, filled at vp_create
 
-// The replicated log table must start at a shared offset aligned to its
-// size (32 KB) so entry offsets can be OR-ed with the lane's copy address.
 template <bool ZERO_CHECK>
-__global__ void __launch_bounds__(FAR_THREADS, 2)
+__global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
     k_far(int64_t T, const double2* __restrict__ txy, int64_t S, const double* __restrict__ sx,
           const double* __restrict__ sy, const double* __restrict__ sq, int64_t chunk,
           double* __restrict__ part, unsigned c3ff) {
   extern __shared__ __align__(16) unsigned char fsm[];
-  // layout: [pad to 32 KB boundary][log table 32 KB][sources]
-  const unsigned sbase = (unsigned)__cvta_generic_to_shared(fsm);
-  const unsigned tab_off = ((sbase + 32767u) & ~32767u) - sbase;
-  double2* tab = (double2*)(fsm + tab_off);
-  double2* sxy = (double2*)(fsm + tab_off + sizeof(LogTab));
-  double* ssq = (double*)(sxy + FAR_TILE);
+  double2* tab = reinterpret_cast<double2*>(fsm);  // kLogEntries x kLogCopies
+  double2* sxy = tab + kLogEntries * kLogCopies;
+  double* ssq = reinterpret_cast<double*>(sxy + FAR_TILE);
   for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += FAR_THREADS) tab[i] = g_logtab[i / kLogCopies];
-  const unsigned lane_tab = sbase + tab_off + 16u * (threadIdx.x & (kLogCopies - 1));
+  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
   const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
   double tx[FAR_R], ty[FAR_R], acc[FAR_R];
 #pragma unroll
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(FAR_THREADS, 2)
       for (int r = 0; r < FAR_R; ++r) {
         const double dx = tx[r] - ps.x, dy = ty[r] - ps.y;
         const double r2 = fma(dx, dx, dy * dy);
-        acc[r] = fma(q, far_log_r2<ZERO_CHECK>(lane_tab, c3ff, r2), acc[r]);
+        acc[r] = fma(q, far_log_r2<ZERO_CHECK>(tab, laneoff, c3ff, r2), acc[r]);
       }
     }
   }
@@ -258,7 +259,6 @@ __global__ void __launch_bounds__(FAR_THREADS, 2)
   }
 }
 
-constexpr size_t kFarSmem = 32768 + sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeof(double));
 
 __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ part,
                              double* __restrict__ u) {
@@ -988,6 +988,8 @@ int compute_sources(vp_ctx* c) {
   c->last_launches += 1;
   return 0;
 }
+
+constexpr size_t kFarSmem = sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeof(double));
 
 int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check) {
   const int64_t S = c->n_tri * c->rules.len_q;

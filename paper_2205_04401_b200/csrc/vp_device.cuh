@@ -161,7 +161,13 @@ __device__ __forceinline__ double density(const CC& cc, double x, double y) {
 // The table {r_k, -log r_k} lives in shared memory, replicated 8x so that
 // the 8 lanes of a quarter-warp hit 8 different bank groups (conflict-free
 // 128-bit loads).  x == 0 (coincident pair) returns 0.
-constexpr int kLogBits = 8;
+#ifndef VP_LOG_BITS
+#define VP_LOG_BITS 9
+#endif
+#ifndef VP_LOG_I2F
+#define VP_LOG_I2F 1
+#endif
+constexpr int kLogBits = VP_LOG_BITS;
 constexpr int kLogEntries = 1 << kLogBits;
 constexpr int kLogCopies = 8;
 
@@ -179,6 +185,33 @@ inline void log_table_fill(double2* host /* kLogEntries */) {
 }
 
 #ifdef __CUDACC__
+// L + log(1 + t) for |t| <= 2^-(kLogBits+1):
+//   8 bits: Taylor degree 5 (truncation 9e-18);
+//   9 bits: minimax degree 4 on [-2^-10, 2^-10] (max error 2.3e-17).
+static_assert(kLogBits == 8 || kLogBits == 9, "log table: 8 or 9 index bits");
+__device__ __forceinline__ double log1p_poly(double t, double L) {
+  if constexpr (kLogBits == 8) {
+    double i = fma(t, 0.2, -0.25);
+    i = fma(t, i, 0.33333333333333333);
+    i = fma(t, i, -0.5);
+    i = fma(t, i, 1.0);
+    return fma(t, i, L);
+  } else {
+    double i = fma(t, -0.25000024181904215854, 0.3333334991010435487);
+    i = fma(t, i, -0.49999999999992096269);
+    i = fma(t, i, 1.0);
+    return fma(t, i, L);
+  }
+}
+
+__device__ __forceinline__ double log_exponent(unsigned hi) {
+  if constexpr (VP_LOG_I2F) {
+    return (double)((int)(hi >> 20) - 1023);
+  } else {
+    return __hiloint2double(0x43380000, (int)(hi >> 20)) - 6755399441056767.0;  // e = biased - 1023
+  }
+}
+
 // base: this lane's copy (tab + (lane & 7) with STRIDE = kLogCopies), or an
 // unreplicated table with STRIDE = 1
 template <int STRIDE>
@@ -186,20 +219,17 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
   const int hi = __double2hiint(x), lo = __double2loint(x);
   const double2 tb = base[((hi >> (20 - kLogBits)) & (kLogEntries - 1)) * STRIDE];
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double ed = __hiloint2double(0x43380000, hi >> 20) - 6755399441056767.0;  // e = biased - 1023
+  const double ed = log_exponent((unsigned)hi);
   const double t = fma(m, tb.x, -1.0);
-  double i = fma(t, 0.2, -0.25);
-  i = fma(t, i, 0.33333333333333333);
-  i = fma(t, i, -0.5);
-  i = fma(t, i, 1.0);
-  const double p = fma(t, i, tb.y);
+  const double p = log1p_poly(t, tb.y);
   const double lg = fma(ed, 0.69314718055994530942, p);
   return hi >= 0x00100000 ? lg : 0.0;
 }
 
 // Far-kernel variant of fast_log_r2 with fewer integer operations:
-//   * `lane_tab` is the byte address (shared window) of this lane's copy of
-//     the replicated table; the entry offset (k*128) is OR-ed in with one LOP3;
+//   * `tab` is the replicated table in *static* shared memory (its address is
+//     a link-time constant folded into the LDS immediate); the entry offset
+//     k*128 and the lane's copy offset (lane&7)*16 are combined by one LOP3;
 //   * the mantissa m is built with one LOP3 using `c3ff` = 0x3ff00000 held in
 //     a register;
 //   * ZERO_CHECK = false skips the r^2 == 0 test.  That is exact for the
@@ -208,21 +238,18 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
 //     function (subtract-and-add), so the finite value
 //     returned for r^2 == 0 cancels.
 template <bool ZERO_CHECK>
-__device__ __forceinline__ double far_log_r2(unsigned lane_tab, unsigned c3ff, double x) {
+__device__ __forceinline__ double far_log_r2(const double2* tab, unsigned laneoff, unsigned c3ff, double x) {
   const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
   unsigned off, mhi;
-  asm("lop3.b32 %0, %1, 0x7f80, %2, 0xEA;" : "=r"(off) : "r"(hi >> 5), "r"(lane_tab));
+  // byte offset of entry k (stride kLogCopies * 16 = 128 B) OR the lane's copy
+  constexpr unsigned kShift = 20 - kLogBits - 7, kMask = (unsigned)(kLogEntries - 1) << 7;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(off) : "r"(hi >> kShift), "n"(kMask), "r"(laneoff));
   asm("lop3.b32 %0, %1, 0x000fffff, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(c3ff));
-  double rk, lk;
-  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(rk), "=d"(lk) : "r"(off));
+  const double2 tb = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + off);
   const double m = __hiloint2double((int)mhi, (int)lo);
-  const double ed = __hiloint2double(0x43380000, (int)(hi >> 20)) - 6755399441056767.0;
-  const double t = fma(m, rk, -1.0);
-  double i = fma(t, 0.2, -0.25);
-  i = fma(t, i, 0.33333333333333333);
-  i = fma(t, i, -0.5);
-  i = fma(t, i, 1.0);
-  const double p = fma(t, i, lk);
+  const double ed = log_exponent(hi);
+  const double t = fma(m, tb.x, -1.0);
+  const double p = log1p_poly(t, tb.y);
   const double lg = fma(ed, 0.69314718055994530942, p);
   if constexpr (ZERO_CHECK) return hi >= 0x00100000u ? lg : 0.0;
   return lg;
