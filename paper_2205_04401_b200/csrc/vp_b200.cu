@@ -200,6 +200,12 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 #ifndef VP_FAR_R
 #define VP_FAR_R 8
 #endif
+#ifndef VP_NEAR_MINB
+#define VP_NEAR_MINB 2
+#endif
+#ifndef VP_SELF_MINB
+#define VP_SELF_MINB 4
+#endif
 #ifndef VP_FAR_MINB
 #define VP_FAR_MINB 2
 #endif
@@ -404,22 +410,34 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-template <int P>
-__device__ __forceinline__ double near_node(const ShCoef& cc, const double2* __restrict__ ltab,
-                                            double2 a, double2 ba, double2 ca, double sc, double2 nxy, double nw,
-                                            double X0, double Y0, double E1x, double E1y, double E2x,
-                                            double E2y, double tx, double ty) {
-  const double xi = fma(nxy.y, ca.x, fma(nxy.x, ba.x, a.x));
-  const double eta = fma(nxy.y, ca.y, fma(nxy.x, ba.y, a.y));
-  const double yx = fma(eta, E2x, fma(xi, E1x, X0));
-  const double yy = fma(eta, E2y, fma(xi, E1y, Y0));
-  const double f = density<P>(cc, xi, eta);
-  const double dx = tx - yx, dy = ty - yy;
-  return (nw * sc) * f * fast_log_r2<1>(ltab, fma(dx, dx, dy * dy));
+// NPT leaf nodes per call share the density coefficient loads
+template <int P, int NPT>
+__device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __restrict__ ltab,
+                                             const double2* a, const double2* ba, const double2* ca,
+                                             const double* sc, const double2* nxy, const double* nw,
+                                             const bool* valid, double X0, double Y0, double E1x,
+                                             double E1y, double E2x, double E2y, double tx, double ty) {
+  double xi[NPT], eta[NPT], f[NPT];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    xi[i] = fma(nxy[i].y, ca[i].x, fma(nxy[i].x, ba[i].x, a[i].x));
+    eta[i] = fma(nxy[i].y, ca[i].y, fma(nxy[i].x, ba[i].y, a[i].y));
+  }
+  density_n<P, NPT>(cc, xi, eta, f);
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const double yx = fma(eta[i], E2x, fma(xi[i], E1x, X0));
+    const double yy = fma(eta[i], E2y, fma(xi[i], E1y, Y0));
+    const double dx = tx - yx, dy = ty - yy;
+    const double v = (nw[i] * sc[i]) * f[i] * fast_log_r2<1>(ltab, fma(dx, dx, dy * dy));
+    acc += valid[i] ? v : 0.0;
+  }
+  return acc;
 }
 
 template <int P>
-__global__ void __launch_bounds__(NEAR_WARPS * 32, 3)
+__global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
     k_near_int(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
                const double2* __restrict__ txy, const ElemRec* __restrict__ el,
                const double* __restrict__ coeffs, const int64_t* __restrict__ loff,
@@ -467,13 +485,22 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, 3)
       }
       __syncwarp();
       const int total = nb * Ln;
-      // node j = (li, ni), lanes strided by 32
+      // nodes j and j + 32 = (li, ni), (lj, nj); lanes strided by 64
       int li = lane / Ln, ni = lane - li * Ln;
-      for (int j = lane; j < total; j += 32) {
-        acc += near_node<P>(ShCoef(cc), sltab, sga[wid][li], sgb[wid][li], sgc[wid][li], sgs[wid][li], snxy[ni],
-                            snw[ni], X0, Y0, E1x, E1y, E2x, E2y, tx, ty);
-        ni += 32;
+      int lj = (lane + 32) / Ln, nj = lane + 32 - lj * Ln;
+      for (int j = lane; j < total; j += 64) {
+        const bool ok2 = j + 32 < total;
+        const int l2 = ok2 ? lj : li, n2 = ok2 ? nj : ni;
+        const double2 ga[2] = {sga[wid][li], sga[wid][l2]}, gb[2] = {sgb[wid][li], sgb[wid][l2]},
+                      gc[2] = {sgc[wid][li], sgc[wid][l2]}, nn[2] = {snxy[ni], snxy[n2]};
+        const double gs[2] = {sgs[wid][li], sgs[wid][l2]}, nwv[2] = {snw[ni], snw[n2]};
+        const bool valid[2] = {true, ok2};
+        acc += near_nodes<P, 2>(ShCoef(cc), sltab, ga, gb, gc, gs, nn, nwv, valid, X0, Y0, E1x, E1y, E2x, E2y,
+                                tx, ty);
+        ni += 64;
         while (ni >= Ln) { ni -= Ln; ++li; }
+        nj += 64;
+        while (nj >= Ln) { nj -= Ln; ++lj; }
       }
     }
     const double val = warp_sum(acc);
@@ -535,7 +562,7 @@ __device__ __forceinline__ double self_bnd(const SelfGeom& G, int i) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(SELF_WARPS * 32, 6)
+__global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
            const double2* __restrict__ txy, const ElemRec* __restrict__ el,
            const double* __restrict__ coeffs, const double* __restrict__ sx,
@@ -612,10 +639,15 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, 6)
         const double lr0 = 0.5 * fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
         const double grx = fma(sl, BRx, Arx) - txi, gry = fma(sl, BRy, Ary) - teta;
         double inner = 0.0;
-        for (int q = 0; q < NG; ++q) {
-          const double rj = sgr[q];
-          const double f = density<P>(ShCoef(cc), fma(rj, grx, txi), fma(rj, gry, teta));
-          inner = fma(sgw[q] * (lr0 + sglr[q]), f, inner);
+        for (int q = 0; q < NG; q += 2) {
+          const int q2 = q + 1 < NG ? q + 1 : q;
+          const double r1 = sgr[q], r2v = sgr[q2];
+          const double xs[2] = {fma(r1, grx, txi), fma(r2v, grx, txi)};
+          const double ys[2] = {fma(r1, gry, teta), fma(r2v, gry, teta)};
+          double f[2];
+          density_n<P, 2>(ShCoef(cc), xs, ys, f);
+          inner = fma(sgw[q] * (lr0 + sglr[q]), f[0], inner);
+          if (q + 1 < NG) inner = fma(sgw[q2] * (lr0 + sglr[q2]), f[1], inner);
         }
         acc = fma(ws * G.h, inner, acc);
       }

@@ -102,55 +102,96 @@ struct ShCoef {
   }
 };
 
-template <int P, int m, int k, class CC>
-__device__ __forceinline__ void jacobi_tail(const CC& cc, double t, double& p0, double& p1, double& s) {
-  if constexpr (m + k + 1 <= P) {
-    constexpr double ja = kc_ja(m, k), jb = kc_jb(m, k), jc = kc_jc(m, k);
-    const double al = fma(ja, t, jb);
-    const double p2 = fma(al, p1, -jc * p0);
-    s = fma(cc[koorn_index(m, m + k + 1)], p2, s);
-    p0 = p1;
-    p1 = p2;
-    jacobi_tail<P, m, k + 1, CC>(cc, t, p0, p1, s);
+// Per m, S_m(t) = sum_k cc[m, m+k] P_k^{(2m+1,0)}(t) by Clenshaw's backward
+// recurrence (b_k = c_k + alpha_k b_{k+1} - beta_{k+1} b_{k+2}, S_m = b_0;
+// alpha_k = ja t + jb, beta_k = jc): 3 FP64 ops per mode.  Then
+// f = sum_m S_m L_m with L_m the homogenised Legendre recurrence.  NPT points
+// share every coefficient load.
+template <int NPT>
+struct Pts {
+  double v[NPT];
+};
+
+template <int P, int m, int k, int NPT, class CC>
+__device__ __forceinline__ void clenshaw_m(const CC& cc, const Pts<NPT>& t, Pts<NPT>& b1, Pts<NPT>& b2) {
+  // processes k = P - m down to 0 for fixed m; on exit b1 = b_0 = S_m
+  if constexpr (k >= 0) {
+    const double c = cc[koorn_index(m, m + k)];
+    if constexpr (k == P - m) {
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        b2.v[i] = 0.0;
+        b1.v[i] = c;
+      }
+    } else {
+      constexpr double a = 2 * m + 1;
+      constexpr double ja = (k == 0) ? 0.5 * (a + 2.0) : kc_ja(m, k);
+      constexpr double jb = (k == 0) ? 0.5 * a : kc_jb(m, k);
+      constexpr double jc1 = kc_jc(m, k + 1);  // beta_{k+1}
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        const double al = fma(ja, t.v[i], jb);
+        double bk = fma(al, b1.v[i], c);
+        if constexpr (k + 2 <= P - m) bk = fma(-jc1, b2.v[i], bk);
+        b2.v[i] = b1.v[i];
+        b1.v[i] = bk;
+      }
+    }
+    clenshaw_m<P, m, k - 1, NPT, CC>(cc, t, b1, b2);
   }
 }
 
-template <int P, int m, class CC>
-__device__ __forceinline__ void koorn_modes(const CC& cc, double t, double u, double v2, double Lm,
-                                            double Lprev, double& f) {
+template <int P, int m, int NPT, class CC>
+__device__ __forceinline__ void koorn_modes_n(const CC& cc, const Pts<NPT>& t, const Pts<NPT>& u,
+                                              const Pts<NPT>& v2, Pts<NPT>& Lm, Pts<NPT>& Lprev,
+                                              Pts<NPT>& f) {
   if constexpr (m <= P) {
-    double s = cc[koorn_index(m, m)];
-    if constexpr (m + 1 <= P) {
-      constexpr double a = 2 * m + 1;
-      constexpr double j1a = 0.5 * (a + 2.0), j1b = 0.5 * a;
-      double p0 = 1.0;
-      double p1 = fma(j1a, t, j1b);
-      s = fma(cc[koorn_index(m, m + 1)], p1, s);
-      jacobi_tail<P, m, 1, CC>(cc, t, p0, p1, s);
-    }
-    f = fma(s, Lm, f);
+    Pts<NPT> b1, b2;
+    clenshaw_m<P, m, P - m, NPT, CC>(cc, t, b1, b2);
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) f.v[i] = fma(b1.v[i], Lm.v[i], f.v[i]);
     if constexpr (m < P) {
-      double Ln;
-      if constexpr (m == 0) {
-        Ln = u;
-      } else {
-        constexpr double la = kc_la(m), lb = kc_lb(m);
-        Ln = fma(la * u, Lm, -lb * v2 * Lprev);
+#pragma unroll
+      for (int i = 0; i < NPT; ++i) {
+        double Ln;
+        if constexpr (m == 0) {
+          Ln = u.v[i];
+        } else {
+          constexpr double la = kc_la(m), lb = kc_lb(m);
+          Ln = fma(la * u.v[i], Lm.v[i], -lb * v2.v[i] * Lprev.v[i]);
+        }
+        Lprev.v[i] = Lm.v[i];
+        Lm.v[i] = Ln;
       }
-      koorn_modes<P, m + 1, CC>(cc, t, u, v2, Ln, Lm, f);
+      koorn_modes_n<P, m + 1, NPT, CC>(cc, t, u, v2, Lm, Lprev, f);
     }
   }
+}
+
+// f at NPT points (x[i], y[i])
+template <int P, int NPT, class CC>
+__device__ __forceinline__ void density_n(const CC& cc, const double* x, const double* y, double* out) {
+  Pts<NPT> t, u, v2, Lm, Lprev, f;
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    const double v = 1.0 - x[i];
+    u.v[i] = fma(2.0, y[i], -v);
+    v2.v[i] = v * v;
+    t.v[i] = fma(2.0, x[i], -1.0);
+    Lm.v[i] = 1.0;
+    Lprev.v[i] = 0.0;
+    f.v[i] = 0.0;
+  }
+  koorn_modes_n<P, 0, NPT, CC>(cc, t, u, v2, Lm, Lprev, f);
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) out[i] = f.v[i];
 }
 
 template <int P, class CC>
 __device__ __forceinline__ double density(const CC& cc, double x, double y) {
-  const double v = 1.0 - x;
-  const double u = fma(2.0, y, -v);
-  const double v2 = v * v;
-  const double t = fma(2.0, x, -1.0);
-  double f = 0.0;
-  koorn_modes<P, 0, CC>(cc, t, u, v2, 1.0, 0.0, f);
-  return f;
+  double o;
+  density_n<P, 1, CC>(cc, &x, &y, &o);
+  return o;
 }
 
 // ---------------------------------------------------------------------------
