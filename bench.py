@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--q", type=int, default=0, help="far order override (config 5 sweep)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--far", choices=["direct", "fmm"], default="direct",
+                    help="far-field method of the headline measurement (north_star: direct)")
+    ap.add_argument("--no-fmm", action="store_true", help="skip the secondary FMM measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-stride", type=int, default=8, help="cpu_baseline target sample stride")
     return ap.parse_args()
@@ -205,6 +208,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     ev = vp.Evaluator(local).load(pr)
+    ev.set_far_method(args.far)
     txy_h = rank_targets(pr, rank, world)
     T = txy_h.shape[0]
     d_txy = torch.from_numpy(txy_h).to(dev).contiguous()
@@ -293,6 +297,37 @@ def main():
                "h2d_bytes_per_step": int(pr.coeffs.nbytes + txy_h.nbytes),
                "d2h_bytes_per_step": int(8 * T)}
 
+    # secondary: the same steps with the other far-field method (FMM)
+    alt = None
+    if not args.no_fmm:
+        other = "fmm" if args.far == "direct" else "direct"
+        u_ref = d_u.clone()
+        ev.set_far_method(other)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a_st, a_ms = [], []
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            a_st.append(step())
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        a_ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+        ta = torch.tensor([a_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        a_ms = float(ta.item())
+        diff = float((d_u - u_ref).abs().max().item() / u_ref.abs().max().item())
+        alt = {"far_method": other, "value": world * T * args.steps / (a_ms * 1e-3),
+               "ms_per_step": a_ms / args.steps,
+               "far_ms": float(np.mean([s["t_far_ms"] for s in a_st])),
+               "fmm_levels": a_st[-1]["fmm_levels"], "fmm_order": 36,
+               "max_rel_diff_u_vs_headline": diff}
+        ev.set_far_method(args.far)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n, dt = cpu_baseline(pr, args.cpu_stride)
@@ -330,6 +365,8 @@ def main():
                          "survey_equiv_tflops": SURVEY_FAR_FLOP_PER_PAIR * T * S / (far_ms * 1e-3) / 1e12,
                          "traffic": prof.get("dram_bytes_per_launch"),
                          "traffic_source": prof.get("source")},
+            "far_method": args.far,
+            "alt_far_method": alt,
             "gpu_launches": int(sum(s["gpu_launches"] for s in stats)),
             "clocks": clocks,
             "e2e": e2e,

@@ -72,6 +72,9 @@ typedef struct {
   double t_total_ms;    /* device time of the whole evaluation */
   double t_sources_ms;  /* device time of K1 alone */
   double t_far_kernel_ms; /* device time of K2 (far sum + its fixed-order reduction) */
+  int32_t far_method;   /* 0 direct, 1 FMM */
+  int32_t fmm_levels;   /* leaf level of the FMM quadtree */
+  int64_t fmm_outside;  /* targets outside the FMM root box (summed directly) */
 } vp_stats;
 
 /* context (device = CUDA ordinal) */
@@ -126,6 +129,12 @@ int vp_near_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
                   double* val, double* sub, int64_t* leaves);
 int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t* elem,
                   double* val, double* sub, int64_t* panels);
+
+/* Far-field method: 0 = direct O(T S) sum (fmm_eval --direct, SPEC.md:618;
+ * the default), 1 = 2-D Laplace FMM (fmm_eval; SURVEY.md
+ * §8(f1)) with expansion order `order` (0 -> 36) and about `leaf_size`
+ * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity. */
+int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 
 /* SM count and compute capability of the context's device. */
 int vp_device_info(vp_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);

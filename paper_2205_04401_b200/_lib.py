@@ -43,6 +43,7 @@ class VpStats(ctypes.Structure):
         ("t_near_ms", ctypes.c_double), ("t_self_ms", ctypes.c_double),
         ("t_total_ms", ctypes.c_double), ("t_sources_ms", ctypes.c_double),
         ("t_far_kernel_ms", ctypes.c_double),
+        ("far_method", ctypes.c_int32), ("fmm_levels", ctypes.c_int32), ("fmm_outside", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -79,6 +80,7 @@ _SIGS = [
                                      c_double_p, c_double_p, c_int64_p]),
     ("vp_self_pairs", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_int32_p,
                                      c_double_p, c_double_p, c_int64_p]),
+    ("vp_set_far_method", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("vp_device_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     # vp_setup.h

@@ -288,6 +288,11 @@ class Evaluator:
         self._rules = rules
         _check(self._L.vp_set_rules(self._h, ctypes.byref(self._rules_struct)), self._err())
 
+    def set_far_method(self, method: str = "direct", order: int = 0, leaf_size: int = 0):
+        """'direct' (O(T S) sum, default) or 'fmm' (2-D Laplace FMM)."""
+        m = {"direct": 0, "fmm": 1}[method]
+        _check(self._L.vp_set_far_method(self._h, m, order, leaf_size), self._err())
+
     def set_density(self, p: int, coeffs):
         c = _f64(coeffs)
         _check(self._L.vp_set_density(self._h, p, _d(c)), self._err())
@@ -370,11 +375,11 @@ def evaluate_field(pr: Problem, targets=None, device: int = 0):
     return u, st
 
 
-def fmm_eval(pr: Problem, targets=None, direct: bool = True, device: int = 0):
-    """fmm_eval -- only the direct O(N^2) path is on the hot
-    path; the FMM itself is the next row."""
-    if not direct:
-        raise UsageError("[1] fmm_eval: only the direct path is implemented (SURVEY.md §8(f1))")
+def fmm_eval(pr: Problem, targets=None, direct: bool = False, order: int = 0, device: int = 0):
+    """fmm_eval: far field of all quadrature-node charges at
+    the targets, by the GPU FMM or, with direct=True, the O(N^2) path."""
     with Evaluator(device) as ev:
         ev.load(pr)
+        if not direct:
+            ev.set_far_method("fmm", order)
         return ev.far_field(pr.txy if targets is None else targets)

@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
 }
 
 
+#include "vp_fmm.cuh"
+
 __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ part,
                              double* __restrict__ u) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -276,17 +278,23 @@ __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ p
 }
 
 // sum_{i in T} q_i log r^2 of element e's sources, warp-cooperative
+// exact_zero = false inside the evaluation: a coincident pair (target = node of
+// its own element) contributes the same finite value here as in the far sum
+// (k_far / k_fmm_eval with ZERO_CHECK=false), so it cancels, as the oracle's
+// skipped pair does.  The per-pair API (vp_near_pairs / vp_self_pairs) uses
+// exact_zero = true so its point sum matches SPEC.md:575 on its own.
 __device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q, double tx,
                                                  double ty, const double* __restrict__ sx,
                                                  const double* __restrict__ sy,
                                                  const double* __restrict__ sq,
-                                                 const double2* __restrict__ ltab) {
+                                                 const double2* __restrict__ ltab, bool exact_zero) {
   double s = 0.0;
   for (int i = lane; i < len_q; i += 32) {
     const int64_t k = e * len_q + i;
     const double dx = tx - sx[k], dy = ty - sy[k];
     const double r2 = fma(dx, dx, dy * dy);
-    s = fma(sq[k], fast_log_r2<1>(ltab, r2), s);
+    const double lg = exact_zero ? fast_log_r2<1, true>(ltab, r2) : fast_log_r2<1, false>(ltab, r2);
+    s = fma(sq[k], lg, s);
   }
   return warp_sum(s);
 }
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
       }
     }
     const double val = warp_sum(acc);
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
     if (lane == 0) {
       if (sub_out) {
         corr[p] = val;
@@ -655,7 +663,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
     const double val = warp_sum(acc) * kInv2Pi;
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
     if (lane == 0) {
       corr[it] = sub_out ? val : val - sub;
       if (sub_out) sub_out[it] = sub;
@@ -775,6 +783,13 @@ struct vp_ctx {
   int64_t n_leaves_last = 0;
   cudaEvent_t ev[8] = {};
   int last_launches = 0;
+  // mesh bounding box (root of the FMM tree)
+  double bx0 = 0, by0 = 0, bx1 = 0, by1 = 0;
+  // far-field method: 0 direct (K2), 1 FMM
+  int far_method = 0, fmm_p = 36, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
+  int64_t fmm_outside = 0;
+  DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
+      f_otxy, f_ou, f_cnt;
 };
 
 namespace {
@@ -1023,7 +1038,15 @@ int compute_sources(vp_ctx* c) {
 
 constexpr size_t kFarSmem = sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeof(double));
 
+int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check, DevBuf& part);
+int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check);
+
 int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check) {
+  if (c->far_method == 1) return fmm_far_sum(c, T, txy, ufar, zero_check);
+  return direct_far_sum(c, T, txy, ufar, zero_check, c->d_part);
+}
+
+int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check, DevBuf& part) {
   const int64_t S = c->n_tri * c->rules.len_q;
   const int64_t tblocks = nblk(T, FAR_THREADS * FAR_R);
   // The source chunking depends on S only, never on T: every target's far
@@ -1032,19 +1055,132 @@ int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_ch
   int64_t chunk = std::max<int64_t>(4096, (S + 63) / 64);
   chunk = (chunk + FAR_TILE - 1) / FAR_TILE * FAR_TILE;
   const int nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
-  CUDA_TRY(c, c->d_part.ensure(sizeof(double) * T * nsplit));
+  CUDA_TRY(c, part.ensure(sizeof(double) * T * nsplit));
   dim3 grid((unsigned)tblocks, (unsigned)nsplit);
   if (zero_check)
     k_far<true><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                          c->d_sq.as<double>(), chunk, c->d_part.as<double>(),
+                                                          c->d_sq.as<double>(), chunk, part.as<double>(),
                                                           0x3ff00000u);
   else
     k_far<false><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                           c->d_sq.as<double>(), chunk, c->d_part.as<double>(),
+                                                           c->d_sq.as<double>(), chunk, part.as<double>(),
                                                            0x3ff00000u);
-  k_far_reduce<<<nblk(T, 256), 256, 0, c->stream>>>(T, nsplit, c->d_part.as<double>(), ufar);
+  k_far_reduce<<<nblk(T, 256), 256, 0, c->stream>>>(T, nsplit, part.as<double>(), ufar);
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 2;
+  return 0;
+}
+
+// FMM far field (vp_fmm.cuh).  The tree is built from the sources only
+// (root = mesh bbox + margin), so u(t) does not depend on the target set.
+int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check) {
+  const int64_t S = c->n_tri * c->rules.len_q;
+  const int p = c->fmm_p, P1 = p + 1;
+  FmmGeom g;
+  const double W = c->bx1 - c->bx0, H = c->by1 - c->by0;
+  g.h0 = std::max(W, H) * (1.0 + 1.0 / 64.0);
+  if (!(g.h0 > 0.0)) g.h0 = 1.0;
+  g.x0 = 0.5 * (c->bx0 + c->bx1) - 0.5 * g.h0;
+  g.y0 = 0.5 * (c->by0 + c->by1) - 0.5 * g.h0;
+  g.p = p;
+  int L = (int)std::lround(0.5 * std::log2(std::max(1.0, (double)S / std::max(1, c->fmm_leaf))));
+  g.L = L = std::max(2, std::min(11, L));
+  c->fmm_levels = L;
+  const int64_t nleaf = 1ll << (2 * L);
+  const int64_t nbox = ((1ll << (2 * (L + 1))) - 1) / 3;
+  FmmTabLayout TL(p);
+  if (c->tab_p != p) {
+    std::vector<double> tab;
+    fmm_tables_fill(p, tab);
+    CUDA_TRY(c, c->f_tab.ensure(sizeof(double) * tab.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->f_tab.p, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->tab_p = p;
+  }
+  // bin and sort the sources by leaf box (stable: source order kept within a box)
+  CUDA_TRY(c, c->f_keys.ensure(sizeof(int32_t) * S));
+  CUDA_TRY(c, c->f_keys2.ensure(sizeof(int32_t) * S));
+  CUDA_TRY(c, c->f_vals.ensure(sizeof(int32_t) * S));
+  CUDA_TRY(c, c->f_idx.ensure(sizeof(int32_t) * S));
+  CUDA_TRY(c, c->f_beg.ensure(sizeof(int64_t) * nleaf));
+  CUDA_TRY(c, c->f_end.ensure(sizeof(int64_t) * nleaf));
+  CUDA_TRY(c, c->f_pxy.ensure(sizeof(double2) * S));
+  CUDA_TRY(c, c->f_pq.ensure(sizeof(double) * S));
+  CUDA_TRY(c, c->f_mp.ensure(sizeof(double2) * nbox * P1));
+  CUDA_TRY(c, c->f_lp.ensure(sizeof(double2) * nbox * P1));
+  k_fmm_keys<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->d_sx.as<double>(), c->d_sy.as<double>(), g,
+                                                   c->f_keys.as<int32_t>(), c->f_vals.as<int32_t>());
+  size_t tmpb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, c->f_keys.as<int32_t>(), c->f_keys2.as<int32_t>(),
+                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->d_tmp.p, tmpb, c->f_keys.as<int32_t>(), c->f_keys2.as<int32_t>(),
+                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->stream);
+  CUDA_TRY(c, cudaMemsetAsync(c->f_beg.p, 0, sizeof(int64_t) * nleaf, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->f_end.p, 0, sizeof(int64_t) * nleaf, c->stream));
+  k_cell_ranges<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->f_keys2.as<int32_t>(), c->f_beg.as<int64_t>(),
+                                                      c->f_end.as<int64_t>());
+  k_fmm_gather<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->f_idx.as<int32_t>(), c->d_sx.as<double>(),
+                                                     c->d_sy.as<double>(), c->d_sq.as<double>(),
+                                                     c->f_pxy.as<double2>(), c->f_pq.as<double>());
+  // upward pass
+  const int wblocks = (int)std::min<int64_t>(nblk(nleaf, kFmmThreads / 32), (int64_t)c->sm_count * 64);
+  k_fmm_p2m<<<std::max(wblocks, 1), kFmmThreads, 0, c->stream>>>(g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(),
+                                                                  c->f_pxy.as<double2>(), c->f_pq.as<double>(),
+                                                                  c->f_mp.as<double2>());
+  const size_t P1e = ((size_t)P1 * P1 + 1) & ~(size_t)1;
+  const size_t sm_m2m = sizeof(double) * (P1e + 8 * P1);
+  for (int l = L - 1; l >= 2; --l) {
+    const int64_t nb = 1ll << (2 * l);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
+    k_fmm_m2m<<<blocks, kFmmThreads, sm_m2m, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>());
+  }
+  // downward pass
+  const size_t sm_m2l = sizeof(double) * (2 * P1e + 8 * P1 + 2 * (kFmmThreads / 32) * P1);
+  for (int l = 2; l <= L; ++l) {
+    const int64_t nb = 1ll << (2 * l);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
+    k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+                                                          c->f_lp.as<double2>());
+  }
+  // L2P + P2P
+  CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
+  const size_t sm_eval = sizeof(LogTab);
+  if (zero_check)
+    k_fmm_eval<true><<<nblk(T, 256), 256, sm_eval, c->stream>>>(
+        T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
+        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
+  else
+    k_fmm_eval<false><<<nblk(T, 256), 256, sm_eval, c->stream>>>(
+        T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
+        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches += 7 + 2 * (L - 1);
+  // targets outside the root box: direct far sum
+  CUDA_TRY(c, c->f_oidx.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_cnt.ensure(sizeof(int64_t)));
+  tmpb = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
+                             c->f_cnt.as<int64_t>(), (int)T, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceSelect::Flagged(c->d_tmp.p, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
+                             c->f_cnt.as<int64_t>(), (int)T, c->stream);
+  int64_t nout = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&nout, c->f_cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->fmm_outside = nout;
+  if (nout > 0) {
+    CUDA_TRY(c, c->f_otxy.ensure(sizeof(double2) * nout));
+    CUDA_TRY(c, c->f_ou.ensure(sizeof(double) * nout));
+    k_gather_targets<<<nblk(nout, 256), 256, 0, c->stream>>>(nout, c->f_oidx.as<int32_t>(), txy,
+                                                              c->f_otxy.as<double2>());
+    if (int rc = direct_far_sum(c, nout, c->f_otxy.as<double2>(), c->f_ou.as<double>(), zero_check, c->d_part))
+      return rc;
+    k_scatter_add<<<nblk(nout, 256), 256, 0, c->stream>>>(nout, c->f_oidx.as<int32_t>(), c->f_ou.as<double>(), ufar);
+    c->last_launches += 2;
+  }
   return 0;
 }
 
@@ -1136,6 +1272,9 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     st->n_outside = T - st->n_self;
     st->n_sources = c->n_tri * c->rules.len_q;
     st->gpu_launches = c->last_launches;
+    st->far_method = c->far_method;
+    st->fmm_levels = c->far_method == 1 ? c->fmm_levels : 0;
+    st->fmm_outside = c->far_method == 1 ? c->fmm_outside : 0;
     float ms[5];
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
     st->t_list_ms = ms[0];
@@ -1191,6 +1330,13 @@ int vp_create(int device, vp_ctx** out) {
     vp_destroy(c);
     return 3;
   }
+  if (cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(k_fmm_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
+    vp_destroy(c);
+    return 3;
+  }
   double2 lt[kLogEntries];
   log_table_fill(lt);
   if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
@@ -1210,6 +1356,18 @@ void vp_destroy(vp_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
+  if (!c) return 1;
+  if (method != 0 && method != 1) return set_err(c, 1, "set_far_method: method must be 0 (direct) or 1 (fmm)");
+  if (order != 0 && (order < 4 || order > kFmmMaxP))
+    return set_err(c, 1, "set_far_method: FMM order must be in [4, 62] (0 = default 36)");
+  if (leaf_size < 0) return set_err(c, 1, "set_far_method: leaf size must be >= 0 (0 = default 40)");
+  c->far_method = method;
+  c->fmm_p = order ? order : 36;
+  c->fmm_leaf = leaf_size ? leaf_size : 40;
+  return 0;
 }
 
 int vp_device_info(vp_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
@@ -1233,6 +1391,14 @@ int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, con
     if (!std::isfinite(vxy[i])) return set_err(c, 2, "set_mesh: non-finite vertex coordinate");
   c->h_vxy.assign(vxy, vxy + 2 * n_vert);
   c->h_tri.assign(tri, tri + 3 * n_tri);
+  c->bx0 = c->by0 = 1e300;
+  c->bx1 = c->by1 = -1e300;
+  for (int64_t i = 0; i < n_vert; ++i) {
+    c->bx0 = std::min(c->bx0, vxy[2 * i]);
+    c->bx1 = std::max(c->bx1, vxy[2 * i]);
+    c->by0 = std::min(c->by0, vxy[2 * i + 1]);
+    c->by1 = std::max(c->by1, vxy[2 * i + 1]);
+  }
   c->n_vert = n_vert;
   c->n_tri = n_tri;
   c->have_mesh = true;

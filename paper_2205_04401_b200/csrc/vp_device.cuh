@@ -255,7 +255,7 @@ __device__ __forceinline__ double log_exponent(unsigned hi) {
 
 // base: this lane's copy (tab + (lane & 7) with STRIDE = kLogCopies), or an
 // unreplicated table with STRIDE = 1
-template <int STRIDE>
+template <int STRIDE, bool ZERO_CHECK = true>
 __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, double x) {
   const int hi = __double2hiint(x), lo = __double2loint(x);
   const double2 tb = base[((hi >> (20 - kLogBits)) & (kLogEntries - 1)) * STRIDE];
@@ -264,7 +264,8 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
   const double t = fma(m, tb.x, -1.0);
   const double p = log1p_poly(t, tb.y);
   const double lg = fma(ed, 0.69314718055994530942, p);
-  return hi >= 0x00100000 ? lg : 0.0;
+  if constexpr (ZERO_CHECK) return hi >= 0x00100000 ? lg : 0.0;
+  return lg;
 }
 
 // Far-kernel variant of fast_log_r2 with fewer integer operations:

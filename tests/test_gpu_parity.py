@@ -238,3 +238,56 @@ def test_config4_full_size_target_sample():
         u_g, _ = ev.evaluate(sample[::40])
     u_o, _, _ = O.evaluate(sample[::40])
     assert rel(u_g, u_o) <= REL_TOL
+
+
+# ---------------------------------------------------------------------------
+# FMM far field: same parity bar as the direct path
+
+@pytest.mark.parametrize("cfg,stride", [(1, 1), (2, 53)])
+def test_fmm_evaluation_matches_oracle(cfg, stride):
+    pr = vp.load_config(cfg)
+    O = Oracle.from_problem(pr)
+    with vp.Evaluator(0) as ev:
+        ev.load(pr)
+        ev.set_far_method("fmm")
+        u_g, st = ev.evaluate(pr.txy)
+        assert st["far_method"] == 1 and st["fmm_levels"] >= 2
+    sub = slice(1, None, stride)
+    u_o, _, _ = O.evaluate(pr.txy[sub])
+    assert rel(u_g[sub], u_o) <= REL_TOL
+
+
+def test_fmm_far_field_outside_targets_and_determinism(cfg2):
+    pr, ev, O = cfg2
+    t = np.vstack([pr.txy[::211], [[5.0, 5.0], [-3.0, 0.25], [0.0, 1.5]]])
+    ev.set_far_method("fmm", 40)
+    try:
+        uf = ev.far_field(t)
+        uf2 = ev.far_field(t)
+        u1, st = ev.evaluate(t)
+        u_half, _ = ev.evaluate(t[: len(t) // 2])
+    finally:
+        ev.set_far_method("direct")
+    assert np.array_equal(uf, uf2)
+    assert np.array_equal(u_half, u1[: len(t) // 2])  # shard invariance (tree from sources only)
+    assert rel(uf, O.far_sum(t)) <= 1e-12
+    assert st["fmm_outside"] >= 2
+
+
+def test_coincident_target_and_source():
+    """A target placed exactly on a far-rule node of its own element: the
+    coincident pair contributes 0 in every path."""
+    pr = vp.load_config(1)
+    O = Oracle.from_problem(pr)
+    with vp.Evaluator(0) as ev:
+        ev.load(pr)
+        sx, sy, _ = ev.sources()
+        t = np.stack([sx[[0, 100, 5000]], sy[[0, 100, 5000]]], 1)
+        t = np.vstack([t, pr.txy[:50]])
+        u_d, _ = ev.evaluate(t)
+        uf_d = ev.far_field(t)
+        ev.set_far_method("fmm")
+        u_f, _ = ev.evaluate(t)
+    u_o, uf_o, _ = O.evaluate(t)
+    assert rel(uf_d, uf_o) <= 1e-13
+    assert rel(u_d, u_o) <= REL_TOL and rel(u_f, u_o) <= REL_TOL
