@@ -136,6 +136,12 @@ int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
  * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity. */
 int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 
+/* Near-leaf density cache: w_i f at the N_n-rule nodes of every sub-simplex
+ * of depth <= max_depth (-1 disables; default 3) is precomputed per element
+ * and shared by all targets, within max_bytes of HBM (0 -> 12 GiB; the depth
+ * is lowered until it fits).  Values match the recurrence to rounding. */
+int vp_set_near_cache(vp_ctx* ctx, int max_depth, int64_t max_bytes);
+
 /* SM count and compute capability of the context's device. */
 int vp_device_info(vp_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 

@@ -293,6 +293,11 @@ class Evaluator:
         m = {"direct": 0, "fmm": 1}[method]
         _check(self._L.vp_set_far_method(self._h, m, order, leaf_size), self._err())
 
+    def set_near_cache(self, max_depth: int = 3, max_bytes: int = 0):
+        """Per-element cache of near-rule densities for sub-simplices of depth
+        <= max_depth (-1 disables)."""
+        _check(self._L.vp_set_near_cache(self._h, max_depth, max_bytes), self._err())
+
     def set_density(self, p: int, coeffs):
         c = _f64(coeffs)
         _check(self._L.vp_set_density(self._h, p, _d(c)), self._err())

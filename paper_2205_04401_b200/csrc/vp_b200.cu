@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "vp.h"
+#include "vp_setup.h"
 #include "vp_device.cuh"
 
 using namespace vp;
@@ -418,6 +419,38 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Per-element cache of w_i f(xi_{slot,i}) at the N_n-rule nodes of every
+// sub-simplex of depth <= D (slot = (4^d - 1)/3 + path): a dense
+// coefficient-to-value contraction G[e][r] = sum_j Vt[j][r] c_e[j] with the
+// host-built Vt[j][r] = w_i K_j(xi_{slot,i}), r = slot * Ln + i.  Each thread
+// owns one row r and 8 elements, so Vt is read once per 8 outputs.
+constexpr int kCacheNE = 8;
+__global__ void __launch_bounds__(256)
+    k_near_cache(int64_t E, int M, int64_t R, const double* __restrict__ Vt, const double* __restrict__ coeffs,
+                 double* __restrict__ out) {
+  __shared__ double sc[kCacheNE][kMaxModes];
+  const int64_t e0 = (int64_t)blockIdx.x * kCacheNE;  // x: element chunks (up to 2^31 - 1)
+  const int ne = (int)min((int64_t)kCacheNE, E - e0);
+  for (int i = threadIdx.x; i < kCacheNE * M; i += blockDim.x) {
+    const int k = i / M, j = i - k * M;
+    sc[k][j] = k < ne ? coeffs[(e0 + k) * M + j] : 0.0;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  double acc[kCacheNE];
+#pragma unroll
+  for (int k = 0; k < kCacheNE; ++k) acc[k] = 0.0;
+  for (int j = 0; j < M; ++j) {
+    const double v = __ldg(Vt + (int64_t)j * R + r);
+#pragma unroll
+    for (int k = 0; k < kCacheNE; ++k) acc[k] = fma(v, sc[k][j], acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < kCacheNE; ++k)
+    if (k < ne) out[(e0 + k) * R + r] = acc[k];
+}
+
 // NPT leaf nodes per call share the density coefficient loads
 template <int P, int NPT>
 __device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __restrict__ ltab,
@@ -451,11 +484,13 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
                const double* __restrict__ coeffs, const int64_t* __restrict__ loff,
                const unsigned long long* __restrict__ leaves, const double* __restrict__ sx,
                const double* __restrict__ sy, const double* __restrict__ sq,
-               const RulesDev* __restrict__ R, double* __restrict__ corr, double* __restrict__ sub_out) {
+               const RulesDev* __restrict__ R, const double* __restrict__ gcache, int cache_depth,
+               double* __restrict__ corr, double* __restrict__ sub_out) {
   constexpr int M = (P + 1) * (P + 2) / 2;
   __shared__ double scc[NEAR_WARPS][M];
   __shared__ double2 sga[NEAR_WARPS][32], sgb[NEAR_WARPS][32], sgc[NEAR_WARPS][32];
   __shared__ double sgs[NEAR_WARPS][32];
+  __shared__ int sslot[NEAR_WARPS][32];
   __shared__ double2 snxy[kMaxNearRule];
   __shared__ double snw[kMaxNearRule];
   __shared__ double2 sltab[kLogEntries];
@@ -477,26 +512,63 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
     const double det = Er.det;
     for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
     const int64_t l0 = loff[p], nl = loff[p + 1] - l0;
+    const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
+    const double* gce = gcache + (int64_t)e * nslot * Ln;
+    const unsigned lt_mask = (1u << lane) - 1u;
     double acc = 0.0;
     for (int64_t lb = 0; lb < nl; lb += 32) {
       const int nb = (int)min((int64_t)32, nl - lb);
       __syncwarp();
-      if (lane < nb) {
-        const unsigned long long code = leaves[l0 + lb + lane];
-        const int d = (int)(code >> 58);
-        double ax, ay, bx, by, cx, cy;
-        decode_path(code & kPathMask, d, ax, ay, bx, by, cx, cy);
-        sga[wid][lane] = make_double2(ax, ay);
-        sgb[wid][lane] = make_double2(bx - ax, by - ay);
-        sgc[wid][lane] = make_double2(cx - ax, cy - ay);
-        sgs[wid][lane] = det * ldexp(1.0, -2 * d) * kInv4Pi;
+      // decode the batch; leaves at depth <= cache_depth go first (their
+      // weighted densities w_i f are read from the per-element cache)
+      bool cached = false;
+      int pos = 0, nc = 0;
+      {
+        unsigned long long code = 0;
+        int d = 0;
+        if (lane < nb) {
+          code = leaves[l0 + lb + lane];
+          d = (int)(code >> 58);
+          cached = d <= cache_depth;
+        }
+        const unsigned cm = __ballot_sync(0xffffffffu, lane < nb && cached);
+        nc = __popc(cm);
+        pos = cached ? __popc(cm & lt_mask) : nc + (lane - __popc(cm & lt_mask));
+        if (lane < nb) {
+          double ax, ay, bx, by, cx, cy;
+          const unsigned long long path = code & kPathMask;
+          decode_path(path, d, ax, ay, bx, by, cx, cy);
+          sga[wid][pos] = make_double2(ax, ay);
+          sgb[wid][pos] = make_double2(bx - ax, by - ay);
+          sgc[wid][pos] = make_double2(cx - ax, cy - ay);
+          sgs[wid][pos] = det * ldexp(1.0, -2 * d) * kInv4Pi;
+          sslot[wid][pos] = cached ? (((1 << (2 * d)) - 1) / 3 + (int)path) : -1;
+        }
       }
       __syncwarp();
+      // (a) cached leaves: r^2 and log only
+      {
+        const int total = nc * Ln;
+        int li = lane / Ln, ni = lane - li * Ln;
+        for (int j = lane; j < total; j += 32) {
+          const double2 a = sga[wid][li], ba = sgb[wid][li], ca = sgc[wid][li], nn = snxy[ni];
+          const double xi = fma(nn.y, ca.x, fma(nn.x, ba.x, a.x));
+          const double eta = fma(nn.y, ca.y, fma(nn.x, ba.y, a.y));
+          const double yx = fma(eta, E2x, fma(xi, E1x, X0));
+          const double yy = fma(eta, E2y, fma(xi, E1y, Y0));
+          const double dx = tx - yx, dy = ty - yy;
+          const double g = __ldg(gce + (int64_t)sslot[wid][li] * Ln + ni);
+          acc = fma(sgs[wid][li] * g, fast_log_r2<1>(sltab, fma(dx, dx, dy * dy)), acc);
+          ni += 32;
+          while (ni >= Ln) { ni -= Ln; ++li; }
+        }
+      }
+      // (b) deeper leaves: density by the Koornwinder recurrence
       const int total = nb * Ln;
       // nodes j and j + 32 = (li, ni), (lj, nj); lanes strided by 64
-      int li = lane / Ln, ni = lane - li * Ln;
-      int lj = (lane + 32) / Ln, nj = lane + 32 - lj * Ln;
-      for (int j = lane; j < total; j += 64) {
+      int li = (nc * Ln + lane) / Ln, ni = nc * Ln + lane - li * Ln;
+      int lj = (nc * Ln + lane + 32) / Ln, nj = nc * Ln + lane + 32 - lj * Ln;
+      for (int j = nc * Ln + lane; j < total; j += 64) {
         const bool ok2 = j + 32 < total;
         const int l2 = ok2 ? lj : li, n2 = ok2 ? nj : ni;
         const double2 ga[2] = {sga[wid][li], sga[wid][l2]}, gb[2] = {sgb[wid][li], sgb[wid][l2]},
@@ -569,32 +641,63 @@ __device__ __forceinline__ double self_bnd(const SelfGeom& G, int i) {
   return G.L;
 }
 
+// Tensor form of the radial-arc-length quadrature.  On the sub-triangle
+// (v, A, B), y(r, sigma) = v + r ((A - v) + sigma (B - A)) (reference
+// coordinates), f(y(r, sigma)) is a polynomial of degree <= p in r and in
+// sigma.  Its tensor Legendre coefficients A_nk follow exactly from (p+1)^2
+// values at Gauss-Legendre points.  The GGQ radial sum of the oracle
+//   sum_j w_j r_j (log r0 + log r_j) f(r_j, sigma)
+// is linear in f, so it equals sum_n beta_n(sigma) (bt_n log r0 + ct_n) with
+// the GGQ-rule moments bt_n = sum_j w_j r_j P_n(2 r_j - 1),
+// ct_n = sum_j w_j r_j log r_j P_n(2 r_j - 1) -- the same rule applied to the
+// same polynomial, for any p.  Contracting with bt/ct once per sub-triangle
+// leaves 2 (p+1)-term Legendre sums per arc-length node instead of N_g + 1
+// density evaluations.
+struct SelfTab {
+  int np;                       // p + 1
+  int pad;
+  double gx[kMaxPdev + 1];      // Gauss-Legendre nodes on [0,1]
+  double PL[(kMaxPdev + 1) * (kMaxPdev + 1)];  // (2n+1) w_a P_n(2 x_a - 1), [n][a]
+  double bt[kMaxPdev + 1], ct[kMaxPdev + 1];   // GGQ-rule moments
+  double la[kMaxPdev + 1], lb[kMaxPdev + 1];   // Legendre recurrence (2k+1)/(k+1), k/(k+1)
+};
+
 template <int P>
 __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
            const double2* __restrict__ txy, const ElemRec* __restrict__ el,
            const double* __restrict__ coeffs, const double* __restrict__ sx,
            const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
-           double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ panels_out,
-           unsigned long long* __restrict__ stats) {
+           const SelfTab* __restrict__ ST, double* __restrict__ corr, double* __restrict__ sub_out,
+           int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats) {
   constexpr int M = (P + 1) * (P + 2) / 2;
-  __shared__ double scc[SELF_WARPS][kMaxModes];
-  __shared__ double sglx[kMaxGL], sglw[kMaxGL], sgr[kMaxGGQ], sgw[kMaxGGQ], sglr[kMaxGGQ];
+  constexpr int NP = P + 1, NP2 = NP * NP;
+  __shared__ double scc[SELF_WARPS][M];
+  __shared__ double sV[SELF_WARPS][NP2], sW[SELF_WARPS][NP2], sE[SELF_WARPS][2 * NP];
+  __shared__ double sPL[NP2], sgx[NP], sbt[NP], sct[NP], sla[NP], slb[NP];
+  __shared__ double sglx[kMaxGL], sglw[kMaxGL];
   __shared__ double2 sltab[kLogEntries];
   for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
-  const int NL = R->n_l, NG = R->n_g1, len_q = R->len_q;
+  const int NL = R->n_l, len_q = R->len_q;
   for (int i = threadIdx.x; i < NL; i += blockDim.x) {
     sglx[i] = R->gl_x[i];
     sglw[i] = R->gl_w[i];
   }
-  for (int i = threadIdx.x; i < NG; i += blockDim.x) {
-    sgr[i] = R->ggq_r[i];
-    sgw[i] = R->ggq_w[i] * R->ggq_r[i];
-    sglr[i] = R->ggq_lr[i];
+  for (int i = threadIdx.x; i < NP2; i += blockDim.x) sPL[i] = ST->PL[i];
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    sgx[i] = ST->gx[i];
+    sbt[i] = ST->bt[i];
+    sct[i] = ST->ct[i];
+    sla[i] = ST->la[i];
+    slb[i] = ST->lb[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* cc = scc[wid];
+  double* V = sV[wid];
+  double* W = sW[wid];
+  double* Eb = sE[wid];
+  double* Ec = sE[wid] + NP;
   unsigned long long my_panels = 0, my_degen = 0;
   for (int64_t it = (int64_t)blockIdx.x * SELF_WARPS + wid; it < n_items;
        it += (int64_t)gridDim.x * SELF_WARPS) {
@@ -613,6 +716,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     const ElemRec& Er = el[e];
     double txi, teta;
     rn_locate(Er, tx, ty, txi, teta);
+    __syncwarp();
     for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
     __syncwarp();
     double acc = 0.0;
@@ -632,6 +736,48 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       }
       const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
       const double BRx = (k == 0 ? 1.0 : 0.0) - Arx, BRy = (k == 1 ? 1.0 : 0.0) - Ary;
+      const double avx = Arx - txi, avy = Ary - teta;  // A - v in reference coordinates
+      // (1) f on the (p+1)^2 Gauss-Legendre grid (r_a, sigma_b), two points per call
+      for (int i = 2 * lane; i < NP2; i += 64) {
+        const int i2 = i + 1 < NP2 ? i + 1 : i;
+        const int a1 = i / NP, b1 = i - a1 * NP, a2 = i2 / NP, b2 = i2 - a2 * NP;
+        const double xs[2] = {fma(sgx[a1], fma(sgx[b1], BRx, avx), txi), fma(sgx[a2], fma(sgx[b2], BRx, avx), txi)};
+        const double ys[2] = {fma(sgx[a1], fma(sgx[b1], BRy, avy), teta), fma(sgx[a2], fma(sgx[b2], BRy, avy), teta)};
+        double f[2];
+        density_n<P, 2>(ShCoef(cc), xs, ys, f);
+        V[i] = f[0];
+        if (i + 1 < NP2) V[i + 1] = f[1];
+      }
+      __syncwarp();
+      // (2) Legendre coefficients in r: W[n][b] = sum_a PL[n][a] V[a][b]
+      for (int o = lane; o < NP2; o += 32) {
+        const int n = o / NP, bb = o - n * NP;
+        double sum = 0.0;
+#pragma unroll
+        for (int aa = 0; aa < NP; ++aa) sum = fma(sPL[n * NP + aa], V[aa * NP + bb], sum);
+        W[o] = sum;
+      }
+      __syncwarp();
+      // (3) and in sigma: A[n][kk] = sum_b PL[kk][b] W[n][b]   (into V)
+      for (int o = lane; o < NP2; o += 32) {
+        const int n = o / NP, kk = o - n * NP;
+        double sum = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < NP; ++bb) sum = fma(sPL[kk * NP + bb], W[n * NP + bb], sum);
+        V[o] = sum;
+      }
+      __syncwarp();
+      // (4) contract the r direction with the GGQ-rule moments
+      for (int o = lane; o < 2 * NP; o += 32) {
+        const int kk = o < NP ? o : o - NP;
+        const double* mom = o < NP ? sbt : sct;
+        double sum = 0.0;
+#pragma unroll
+        for (int n = 0; n < NP; ++n) sum = fma(V[n * NP + kk], mom[n], sum);
+        sE[wid][o] = sum;
+      }
+      __syncwarp();
+      // (5) arc-length nodes: dyadic panels x Gauss-Legendre
       const int nodes = G.npan * NL;
       const double invL = 1.0 / G.L;
       for (int j = lane; j < nodes; j += 32) {
@@ -645,20 +791,24 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         const double px = fma(sl, G.ABx, G.Ax), py = fma(sl, G.ABy, G.Ay);
         const double ddx = px - tx, ddy = py - ty;
         const double lr0 = 0.5 * fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
-        const double grx = fma(sl, BRx, Arx) - txi, gry = fma(sl, BRy, Ary) - teta;
-        double inner = 0.0;
-        for (int q = 0; q < NG; q += 2) {
-          const int q2 = q + 1 < NG ? q + 1 : q;
-          const double r1 = sgr[q], r2v = sgr[q2];
-          const double xs[2] = {fma(r1, grx, txi), fma(r2v, grx, txi)};
-          const double ys[2] = {fma(r1, gry, teta), fma(r2v, gry, teta)};
-          double f[2];
-          density_n<P, 2>(ShCoef(cc), xs, ys, f);
-          inner = fma(sgw[q] * (lr0 + sglr[q]), f[0], inner);
-          if (q + 1 < NG) inner = fma(sgw[q2] * (lr0 + sglr[q2]), f[1], inner);
+        const double x = fma(2.0, sl, -1.0);
+        double q0 = 1.0, q1 = x;
+        double ib = Eb[0], ic = Ec[0];
+        if (NP > 1) {
+          ib = fma(Eb[1], q1, ib);
+          ic = fma(Ec[1], q1, ic);
         }
-        acc = fma(ws * G.h, inner, acc);
+#pragma unroll
+        for (int kk = 1; kk + 1 < NP; ++kk) {
+          const double q2 = fma(sla[kk] * x, q1, -slb[kk] * q0);
+          ib = fma(Eb[kk + 1], q2, ib);
+          ic = fma(Ec[kk + 1], q2, ic);
+          q0 = q1;
+          q1 = q2;
+        }
+        acc = fma(ws * G.h, fma(lr0, ib, ic), acc);
       }
+      __syncwarp();
       for (int pi = 0; pi < G.npan; ++pi)
         if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
@@ -788,6 +938,13 @@ struct vp_ctx {
   // far-field method: 0 direct (K2), 1 FMM
   int far_method = 0, fmm_p = 36, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
   int64_t fmm_outside = 0;
+  DevBuf d_selftab;
+  int selftab_p = -1;
+  // near-leaf density cache (depth <= cache_depth sub-simplices), see k_near_cache
+  int cache_max_depth = 3, cache_depth = -1;
+  int64_t cache_max_bytes = 12ll << 30;
+  DevBuf d_cacheV, d_gcache;
+  int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
 };
@@ -968,8 +1125,11 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
   k_near_int<P><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
       c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-      c->d_rules.as<RulesDev>(), corr, sub);
+      c->d_rules.as<RulesDev>(), c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr, c->cache_depth, corr,
+      sub);
 }
+
+int build_near_cache(vp_ctx* c);
 
 int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
                 double* corr, double* sub, int64_t* leaves_host) {
@@ -992,6 +1152,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   k_near_leaves<true><<<nblk(n, 128), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
       c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+  if (int rc = build_near_cache(c)) return rc;
   VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub);
   CUDA_TRY(c, cudaGetLastError());
   c->n_leaves_last = nleaves;
@@ -1007,10 +1168,117 @@ void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem
   const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
   k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
-      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
-      c->d_stats.as<unsigned long long>());
+      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
+      sub, panels, c->d_stats.as<unsigned long long>());
 }
 
+
+// host decode of a sub-simplex path (same child order as decode_path)
+static void host_decode_path(unsigned long long path, int d, double v[6]) {
+  double ax = 0, ay = 0, bx = 1, by = 0, cx = 0, cy = 1;
+  for (int l = d - 1; l >= 0; --l) {
+    const int ch = (int)((path >> (2 * l)) & 3ull);
+    const double abx = (ax + bx) * 0.5, aby = (ay + by) * 0.5, bcx = (bx + cx) * 0.5, bcy = (by + cy) * 0.5;
+    const double cax = (cx + ax) * 0.5, cay = (cy + ay) * 0.5;
+    if (ch == 0) { bx = abx; by = aby; cx = cax; cy = cay; }
+    else if (ch == 1) { ax = abx; ay = aby; cx = bcx; cy = bcy; }
+    else if (ch == 2) { ax = cax; ay = cay; bx = bcx; by = bcy; }
+    else { ax = bcx; ay = bcy; bx = cax; by = cay; cx = abx; cy = aby; }
+  }
+  v[0] = ax; v[1] = ay; v[2] = bx; v[3] = by; v[4] = cx; v[5] = cy;
+}
+
+// Build (per evaluation) the per-element near-leaf cache: choose the depth
+// D <= cache_max_depth whose cache fits cache_max_bytes, build Vt on the host
+// once per (p, rules, D), then contract on the device.
+int build_near_cache(vp_ctx* c) {
+  const int Ln = c->rules.len_n, M = c->M;
+  int D = std::min(c->cache_max_depth, 6);
+  while (D >= 0) {
+    const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3;
+    if ((double)c->n_tri * nslot * Ln * 8.0 <= (double)c->cache_max_bytes) break;
+    --D;
+  }
+  c->cache_depth = D;
+  if (D < 0) return 0;
+  const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3, R = nslot * Ln;
+  if (c->cacheV_depth != D || c->cacheV_p != c->p) {
+    std::vector<double> Vt((size_t)M * R), kv(M);
+    const vp_rules& r = c->rules;
+    for (int d = 0; d <= D; ++d) {
+      const int64_t off = ((1ll << (2 * d)) - 1) / 3, n = 1ll << (2 * d);
+      for (int64_t path = 0; path < n; ++path) {
+        double v[6];
+        host_decode_path((unsigned long long)path, d, v);
+        for (int i = 0; i < Ln; ++i) {
+          const double u = r.near_x[i], w = r.near_y[i];
+          const double xi = v[0] + (u * (v[2] - v[0]) + w * (v[4] - v[0]));
+          const double eta = v[1] + (u * (v[3] - v[1]) + w * (v[5] - v[1]));
+          koorn_eval(c->p, xi, eta, kv.data());
+          const int64_t row = (off + path) * Ln + i;
+          for (int j = 0; j < M; ++j) Vt[(size_t)j * R + row] = r.near_w[i] * kv[j];
+        }
+      }
+    }
+    CUDA_TRY(c, c->d_cacheV.ensure(sizeof(double) * Vt.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_cacheV.p, Vt.data(), sizeof(double) * Vt.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->cacheV_depth = D;
+    c->cacheV_p = c->p;
+  }
+  CUDA_TRY(c, c->d_gcache.ensure(sizeof(double) * (size_t)(c->n_tri * R)));
+  if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
+  dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
+  k_near_cache<<<grid, 256, 0, c->stream>>>(c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(),
+                                            c->d_gcache.as<double>());
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_launches += 1;
+  return 0;
+}
+
+// SelfTab for the current (p, GGQ rule): Gauss-Legendre interpolation grid
+// on [0,1], Legendre projection weights and the GGQ-rule moments.
+int upload_self_tab(vp_ctx* c) {
+  if (!c->have_rules || c->p < 0) return 0;
+  SelfTab T;
+  std::memset(&T, 0, sizeof(T));
+  const int np = c->p + 1;
+  T.np = np;
+  double gx[kMaxPdev + 1], gw[kMaxPdev + 1];
+  if (vps_gauss_legendre(np, gx, gw) != 0) return set_err(c, 1, "self table: Gauss-Legendre failed");
+  auto legendre = [](int n, double x) {
+    double p0 = 1.0, p1 = x;
+    if (n == 0) return 1.0;
+    for (int k = 1; k < n; ++k) {
+      const double p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+      p0 = p1;
+      p1 = p2;
+    }
+    return p1;
+  };
+  for (int a = 0; a < np; ++a) T.gx[a] = 0.5 * (gx[a] + 1.0);
+  for (int n = 0; n < np; ++n)
+    for (int a = 0; a < np; ++a) T.PL[n * np + a] = (2 * n + 1) * (0.5 * gw[a]) * legendre(n, gx[a]);
+  const vp_rules& r = c->rules;
+  for (int n = 0; n < np; ++n) {
+    double b = 0.0, cc = 0.0;
+    for (int j = 0; j <= r.n_g; ++j) {
+      const double rj = r.ggq_r[j], wj = r.ggq_w[j], pn = legendre(n, 2.0 * rj - 1.0);
+      b += wj * rj * pn;
+      cc += wj * rj * std::log(rj) * pn;
+    }
+    T.bt[n] = b;
+    T.ct[n] = cc;
+    T.la[n] = double(2 * n + 1) / double(n + 1);
+    T.lb[n] = double(n) / double(n + 1);
+  }
+  CUDA_TRY(c, c->d_selftab.ensure(sizeof(SelfTab)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_selftab.p, &T, sizeof(SelfTab), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->selftab_p = c->p;
+  return 0;
+}
 
 int ensure_ready(vp_ctx* c, bool need_density) {
   if (!c) return 1;
@@ -1358,6 +1626,15 @@ void vp_destroy(vp_ctx* c) {
   delete c;
 }
 
+int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
+  if (!c) return 1;
+  if (max_depth < -1 || max_depth > 6) return set_err(c, 1, "set_near_cache: max_depth must be in [-1, 6]");
+  if (max_bytes < 0) return set_err(c, 1, "set_near_cache: max_bytes must be >= 0");
+  c->cache_max_depth = max_depth;
+  c->cache_max_bytes = max_bytes ? max_bytes : (12ll << 30);
+  return 0;
+}
+
 int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
   if (!c) return 1;
   if (method != 0 && method != 1) return set_err(c, 1, "set_far_method: method must be 0 (direct) or 1 (fmm)");
@@ -1468,8 +1745,10 @@ int vp_set_rules(vp_ctx* c, const vp_rules* r) {
   CUDA_TRY(c, cudaMemcpyAsync(c->d_rules.p, &d, sizeof(RulesDev), cudaMemcpyHostToDevice, c->stream));
   c->have_rules = true;
   c->sources_valid = false;
+  c->cacheV_depth = -2;
   if (c->have_mesh)
     if (int rc = build_elements(c)) return rc;
+  if (int rc = upload_self_tab(c)) return rc;
   if (c->p >= 0) {  // Koornwinder values at the far nodes for K1
     const int M = koorn_size(c->p);
     std::vector<double> V((size_t)r->len_q * M);
@@ -1502,7 +1781,8 @@ int vp_set_density(vp_ctx* c, int p, const double* coeffs) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->have_density = true;
   c->sources_valid = false;
-  return 0;
+  c->cacheV_depth = -2;
+  return upload_self_tab(c);
 }
 
 int vp_build_nearlist(vp_ctx* c, int64_t n_tgt, const double* txy, int32_t* self_out, int64_t* offsets_out,

@@ -291,3 +291,26 @@ def test_coincident_target_and_source():
     u_o, uf_o, _ = O.evaluate(t)
     assert rel(uf_d, uf_o) <= 1e-13
     assert rel(u_d, u_o) <= REL_TOL and rel(u_f, u_o) <= REL_TOL
+
+
+@pytest.mark.parametrize("depth", [-1, 0, 1, 3])
+def test_near_cache_depths_match_oracle(cfg2, depth):
+    """The per-element near-leaf density cache (any depth, or off) leaves the
+    near corrections at oracle parity and the leaf counts unchanged."""
+    pr, ev, O = cfg2
+    s, off, ids = O.nearlist(pr.txy[::151])
+    ts = np.repeat(np.arange(len(s)), np.diff(off))
+    pick = np.linspace(0, len(ids) - 1, 120).astype(int)
+    t = pr.txy[::151][ts[pick]]
+    ev.set_near_cache(depth)
+    try:
+        val, sub, lv = ev.near_pairs(t, ids[pick])
+        u, _ = ev.evaluate(pr.txy[::97])
+    finally:
+        ev.set_near_cache(3)
+    ref = np.array([O.near_pair(x, y, e) for (x, y), e in zip(t, ids[pick])])
+    scale = np.abs(ref[:, 1]).max()
+    assert np.abs(val - ref[:, 0]).max() <= 1e-13 * scale
+    assert np.array_equal(lv, ref[:, 2].astype(np.int64))
+    u_o, _, _ = O.evaluate(pr.txy[::97])
+    assert rel(u, u_o) <= REL_TOL
