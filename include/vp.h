@@ -136,6 +136,21 @@ int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
  * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity. */
 int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 
+/* Potential interpolation.  interp_coeffs (rules.hpp:
+ * 165-170): per-element Koornwinder coefficients [n_elem * M_p] from values
+ * at the M_p reference nodes (ref_x, ref_y) of an interpolation rule, e.g.
+ * u at the element's targets; *cond receives the infinity-norm condition
+ * number of the Vandermonde (make_interp_rule, rules.hpp:139-156). */
+int vp_interp_coeffs(vp_ctx* ctx, int p, const double* ref_x, const double* ref_y, int64_t n_elem,
+                     const double* values, double* coeffs, double* cond);
+
+/* field_eval: evaluate the PotentialField (interpolation
+ * mesh + coefficients) at points; points outside every element give NaN,
+ * elem_out = -1 and are counted in *n_outside. */
+int vp_field_eval(vp_ctx* ctx, int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri,
+                  int p, const double* coeffs, int64_t n_pts, const double* pts, double* out,
+                  int32_t* elem_out, int64_t* n_outside);
+
 /* Near-leaf density cache: w_i f at the N_n-rule nodes of every sub-simplex
  * of depth <= max_depth (-1 disables; default 3) is precomputed per element
  * and shared by all targets, within max_bytes of HBM (0 -> 12 GiB; the depth

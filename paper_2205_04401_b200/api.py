@@ -358,6 +358,32 @@ class Evaluator:
         _check(fn(self._h, n, _d(t), _i32(e), _d(val), _d(sub), _i64(cnt)), self._err())
         return val, sub, cnt
 
+    def interp_coeffs(self, p: int, ref_x, ref_y, values):
+        """Per-element Koornwinder coefficients from values at the M_p reference
+        nodes (interp_coeffs, rules.hpp:165-170); returns (coeffs, condition)."""
+        rx, ry = _f64(ref_x), _f64(ref_y)
+        v = _f64(values).reshape(-1, koorn_size(p))
+        out = np.zeros_like(v)
+        cond = ctypes.c_double()
+        _check(self._L.vp_interp_coeffs(self._h, p, _d(rx), _d(ry), v.shape[0], _d(v), _d(out),
+                                        ctypes.byref(cond)), self._err())
+        return out, cond.value
+
+    def field_eval(self, vxy, tri, p: int, coeffs, pts, allow_outside: bool = False):
+        """Evaluate a PotentialField at points (field_eval)."""
+        v = _f64(vxy, (-1, 2))
+        t = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
+        c = _f64(coeffs)
+        x = _f64(pts, (-1, 2))
+        out = np.zeros(x.shape[0])
+        eo = np.zeros(x.shape[0], dtype=np.int32)
+        nout = ctypes.c_int64()
+        _check(self._L.vp_field_eval(self._h, v.shape[0], _d(v), t.shape[0], _i32(t), p, _d(c), x.shape[0],
+                                     _d(x), _d(out), _i32(eo), ctypes.byref(nout)), self._err())
+        if nout.value and not allow_outside:
+            raise NumericalError(f"[2] field_eval: {nout.value} point(s) outside domain")
+        return out, eo
+
     def near_pairs(self, txy, elem):
         """near_eval(T, t), the point sum it replaces, and leaf counts."""
         return self._pairs(self._L.vp_near_pairs, txy, elem)

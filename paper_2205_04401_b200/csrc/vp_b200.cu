@@ -830,6 +830,125 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   if (lane == 0 && my_degen) atomicAdd(&stats[4], my_degen);
 }
 
+// ---------------------------------------------------------------------------
+// Potential interpolation (rules.hpp:129-170 InterpRule /
+// interp_coeffs; SPEC.md:566-569, :592-600 PotentialField / field_eval).
+// coeffs[e][j] = sum_k Vinv[j][k] values[e][k]: a batched [M x M] x [M x E]
+// contraction with the inverse Koornwinder Vandermonde of the interpolation
+// nodes; each thread owns one output row j for 8 elements.
+__global__ void __launch_bounds__(128)
+    k_interp(int64_t E, int M, const double* __restrict__ Vinv, const double* __restrict__ vals,
+             double* __restrict__ out) {
+  __shared__ double sv[kCacheNE][kMaxModes];
+  const int64_t e0 = (int64_t)blockIdx.x * kCacheNE;
+  const int ne = (int)min((int64_t)kCacheNE, E - e0);
+  for (int i = threadIdx.x; i < kCacheNE * M; i += blockDim.x) {
+    const int k = i / M, j = i - k * M;
+    sv[k][j] = k < ne ? vals[(e0 + k) * M + j] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    double acc[kCacheNE];
+#pragma unroll
+    for (int k = 0; k < kCacheNE; ++k) acc[k] = 0.0;
+    for (int kk = 0; kk < M; ++kk) {
+      const double v = __ldg(Vinv + (int64_t)j * M + kk);
+#pragma unroll
+      for (int k = 0; k < kCacheNE; ++k) acc[k] = fma(v, sv[k][kk], acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kCacheNE; ++k)
+      if (k < ne) out[(e0 + k) * M + j] = acc[k];
+  }
+}
+
+// field_eval: locate each point in the interpolation mesh (barycentric, tol
+// 1e-12, lowest id; candidates from a uniform grid of triangle bboxes) and
+// evaluate the element's Koornwinder expansion at the point's reference
+// coordinates.  Points outside every element get NaN and elem = -1.
+struct TriBox {
+  double x0, y0, i00, i01, i10, i11;
+};
+
+__global__ void k_tri_boxes(int64_t E, const double2* __restrict__ v, const int32_t* __restrict__ tri,
+                            TriBox* __restrict__ tb, double4* __restrict__ bb) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double2 a = v[tri[3 * e]], b = v[tri[3 * e + 1]], c = v[tri[3 * e + 2]];
+  const double e1x = b.x - a.x, e1y = b.y - a.y, e2x = c.x - a.x, e2y = c.y - a.y;
+  const double det = e1x * e2y - e2x * e1y;
+  tb[e] = TriBox{a.x, a.y, e2y / det, -e2x / det, -e1y / det, e1x / det};
+  const double pad = 1e-9 * (fabs(e1x) + fabs(e1y) + fabs(e2x) + fabs(e2y));
+  bb[e] = make_double4(fmin(a.x, fmin(b.x, c.x)) - pad, fmin(a.y, fmin(b.y, c.y)) - pad,
+                       fmax(a.x, fmax(b.x, c.x)) + pad, fmax(a.y, fmax(b.y, c.y)) + pad);
+}
+
+__global__ void k_box_count(int64_t E, const double4* __restrict__ bb, GridDev g, int64_t* __restrict__ cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double4 b = bb[e];
+  const int cx0 = cell_coord(b.x, g.x0, g.inv_cs, g.nx), cx1 = cell_coord(b.z, g.x0, g.inv_cs, g.nx);
+  const int cy0 = cell_coord(b.y, g.y0, g.inv_cs, g.ny), cy1 = cell_coord(b.w, g.y0, g.inv_cs, g.ny);
+  cnt[e] = (int64_t)(cx1 - cx0 + 1) * (cy1 - cy0 + 1);
+}
+
+__global__ void k_box_fill(int64_t E, const double4* __restrict__ bb, GridDev g, const int64_t* __restrict__ off,
+                           int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const double4 b = bb[e];
+  const int cx0 = cell_coord(b.x, g.x0, g.inv_cs, g.nx), cx1 = cell_coord(b.z, g.x0, g.inv_cs, g.nx);
+  const int cy0 = cell_coord(b.y, g.y0, g.inv_cs, g.ny), cy1 = cell_coord(b.w, g.y0, g.inv_cs, g.ny);
+  int64_t o = off[e];
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      keys[o] = cy * g.nx + cx;
+      vals[o] = (int32_t)e;
+      ++o;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(128)
+    k_field_eval(int64_t n, const double2* __restrict__ pts, const TriBox* __restrict__ tb,
+                 const double4* __restrict__ bb, GridDev g, const int64_t* __restrict__ cbeg,
+                 const int64_t* __restrict__ cend, const int32_t* __restrict__ celems,
+                 const double* __restrict__ coeffs, double* __restrict__ out, int32_t* __restrict__ elem_out) {
+  constexpr int M = (P + 1) * (P + 2) / 2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 z = pts[i];
+  const double fx = floor(rn_mul(rn_sub(z.x, g.x0), g.inv_cs)), fy = floor(rn_mul(rn_sub(z.y, g.y0), g.inv_cs));
+  int32_t found = -1;
+  double xi = 0.0, eta = 0.0;
+  if (fx >= 0.0 && fy >= 0.0 && fx < (double)g.nx && fy < (double)g.ny) {
+    const int c = (int)fy * g.nx + (int)fx;
+    for (int64_t k = cbeg[c]; k < cend[c] && found < 0; ++k) {
+      const int32_t e = celems[k];
+      const double4 b = bb[e];
+      if (!(z.x >= b.x && z.x <= b.z && z.y >= b.y && z.y <= b.w)) continue;
+      const TriBox T = tb[e];
+      const double dx = rn_sub(z.x, T.x0), dy = rn_sub(z.y, T.y0);
+      const double a = rn_add(rn_mul(T.i00, dx), rn_mul(T.i01, dy));
+      const double bq = rn_add(rn_mul(T.i10, dx), rn_mul(T.i11, dy));
+      const double l0 = rn_sub(rn_sub(1.0, a), bq);
+      if (a >= -kBaryTol && bq >= -kBaryTol && l0 >= -kBaryTol) {
+        found = e;
+        xi = fmin(fmax(a, 0.0), 1.0);
+        eta = fmin(fmax(bq, 0.0), 1.0 - xi);
+      }
+    }
+  }
+  elem_out[i] = found;
+  if (found < 0) {
+    out[i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double cc[M];
+  for (int j = 0; j < M; ++j) cc[j] = coeffs[(int64_t)found * M + j] * c_cn[j];
+  out[i] = density<P>(cc, xi, eta);
+}
+
 __global__ void k_assemble(int64_t T, const double* __restrict__ ufar, const int64_t* __restrict__ off,
                            const double* __restrict__ corr, const double* __restrict__ corr_self,
                            double* __restrict__ u) {
@@ -1920,6 +2039,174 @@ static int pairs_common(vp_ctx* c, int64_t n, const double* txy, const int32_t* 
   CUDA_TRY(c, cudaMemcpyAsync(&herr, c->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (herr) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits");
+  return 0;
+}
+
+// interp_coeffs (rules.hpp:165-170) batched on the device: the inverse
+// Vandermonde of the interpolation nodes is formed on the host by Gauss-Jordan
+// elimination with partial pivoting (make_interp_rule, rules.hpp:139-156).
+int vp_interp_coeffs(vp_ctx* c, int p, const double* ref_x, const double* ref_y, int64_t n_elem,
+                     const double* values, double* coeffs, double* cond) {
+  if (!c) return 1;
+  if (p < 0 || p > kMaxPdev) return set_err(c, 1, "interp_coeffs: order p must be in [0, 12]");
+  if (n_elem <= 0 || !ref_x || !ref_y || !values || !coeffs)
+    return set_err(c, 1, "interp_coeffs: value count must equal rule length (empty input)");
+  const int M = koorn_size(p);
+  std::vector<double> V((size_t)M * M), A((size_t)M * 2 * M, 0.0);
+  for (int i = 0; i < M; ++i) {
+    if (ref_x[i] < -1e-9 || ref_y[i] < -1e-9 || ref_x[i] + ref_y[i] > 1 + 1e-9)
+      return set_err(c, 2, "interp_coeffs: node outside the simplex");
+    koorn_eval(p, ref_x[i], ref_y[i], &V[(size_t)i * M]);
+  }
+  for (int i = 0; i < M; ++i) {
+    for (int j = 0; j < M; ++j) A[(size_t)i * 2 * M + j] = V[(size_t)i * M + j];
+    A[(size_t)i * 2 * M + M + i] = 1.0;
+  }
+  for (int col = 0; col < M; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < M; ++r)
+      if (std::abs(A[(size_t)r * 2 * M + col]) > std::abs(A[(size_t)piv * 2 * M + col])) piv = r;
+    if (!(std::abs(A[(size_t)piv * 2 * M + col]) > 0.0))
+      return set_err(c, 2, "interp_coeffs: nodes are not unisolvent (singular Vandermonde)");
+    if (piv != col)
+      for (int k = 0; k < 2 * M; ++k) std::swap(A[(size_t)col * 2 * M + k], A[(size_t)piv * 2 * M + k]);
+    const double d = A[(size_t)col * 2 * M + col];
+    for (int k = 0; k < 2 * M; ++k) A[(size_t)col * 2 * M + k] /= d;
+    for (int r = 0; r < M; ++r) {
+      if (r == col) continue;
+      const double f = A[(size_t)r * 2 * M + col];
+      if (f == 0.0) continue;
+      for (int k = 0; k < 2 * M; ++k) A[(size_t)r * 2 * M + k] -= f * A[(size_t)col * 2 * M + k];
+    }
+  }
+  std::vector<double> Vinv((size_t)M * M);
+  double nv = 0.0, ni = 0.0;  // infinity-norm condition number estimate
+  for (int i = 0; i < M; ++i) {
+    double rv = 0.0, ri = 0.0;
+    for (int j = 0; j < M; ++j) {
+      Vinv[(size_t)i * M + j] = A[(size_t)i * 2 * M + M + j];
+      rv += std::abs(V[(size_t)i * M + j]);
+      ri += std::abs(Vinv[(size_t)i * M + j]);
+    }
+    nv = std::max(nv, rv);
+    ni = std::max(ni, ri);
+  }
+  if (cond) *cond = nv * ni;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DevBuf dV, dvals, dout;
+  CUDA_TRY(c, dV.ensure(sizeof(double) * Vinv.size()));
+  CUDA_TRY(c, dvals.ensure(sizeof(double) * n_elem * M));
+  CUDA_TRY(c, dout.ensure(sizeof(double) * n_elem * M));
+  CUDA_TRY(c, cudaMemcpyAsync(dV.p, Vinv.data(), sizeof(double) * Vinv.size(), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dvals.p, values, sizeof(double) * n_elem * M, cudaMemcpyHostToDevice, c->stream));
+  k_interp<<<nblk(n_elem, kCacheNE), 128, 0, c->stream>>>(n_elem, M, dV.as<double>(), dvals.as<double>(),
+                                                          dout.as<double>());
+  CUDA_TRY(c, cudaGetLastError());
+  CUDA_TRY(c, cudaMemcpyAsync(coeffs, dout.p, sizeof(double) * n_elem * M, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+extern "C++" {
+template <int P>
+void launch_field_eval(vp_ctx* c, int64_t n, const double2* pts, const TriBox* tb, const double4* bb, GridDev g,
+                       const int64_t* cb, const int64_t* ce, const int32_t* cel, const double* coeffs, double* out,
+                       int32_t* eo) {
+  k_field_eval<P><<<nblk(n, 128), 128, 0, c->stream>>>(n, pts, tb, bb, g, cb, ce, cel, coeffs, out, eo);
+}
+}
+
+int vp_field_eval(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri, int p,
+                  const double* coeffs, int64_t n_pts, const double* pts, double* out, int32_t* elem_out,
+                  int64_t* n_outside) {
+  if (!c) return 1;
+  if (n_vert <= 0 || n_tri <= 0 || !vxy || !tri) return set_err(c, 1, "field_eval: empty interpolation mesh");
+  if (p < 0 || p > kMaxPdev || !coeffs) return set_err(c, 1, "field_eval: order p must be in [0, 12]");
+  if (n_pts < 0 || (n_pts > 0 && (!pts || !out))) return set_err(c, 1, "field_eval: bad point array");
+  for (int64_t i = 0; i < 3 * n_tri; ++i)
+    if (tri[i] < 0 || tri[i] >= n_vert) return set_err(c, 1, "field_eval: triangle vertex index out of range");
+  if (n_pts == 0) {
+    if (n_outside) *n_outside = 0;
+    return 0;
+  }
+  const int M = koorn_size(p);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DevBuf dv, dt, dtb, dbb, dcf, dp, dout, deo, cnt, off, keys, vals, keys2, cel, cb, ce;
+  CUDA_TRY(c, dv.ensure(sizeof(double) * 2 * n_vert));
+  CUDA_TRY(c, dt.ensure(sizeof(int32_t) * 3 * n_tri));
+  CUDA_TRY(c, dtb.ensure(sizeof(TriBox) * n_tri));
+  CUDA_TRY(c, dbb.ensure(sizeof(double4) * n_tri));
+  CUDA_TRY(c, dcf.ensure(sizeof(double) * n_tri * M));
+  CUDA_TRY(c, dp.ensure(sizeof(double) * 2 * n_pts));
+  CUDA_TRY(c, dout.ensure(sizeof(double) * n_pts));
+  CUDA_TRY(c, deo.ensure(sizeof(int32_t) * n_pts));
+  CUDA_TRY(c, cudaMemcpyAsync(dv.p, vxy, sizeof(double) * 2 * n_vert, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dt.p, tri, sizeof(int32_t) * 3 * n_tri, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dcf.p, coeffs, sizeof(double) * n_tri * M, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dp.p, pts, sizeof(double) * 2 * n_pts, cudaMemcpyHostToDevice, c->stream));
+  k_tri_boxes<<<nblk(n_tri, 256), 256, 0, c->stream>>>(n_tri, dv.as<double2>(), dt.as<int32_t>(), dtb.as<TriBox>(),
+                                                        dbb.as<double4>());
+  // grid: cell = mean triangle extent, from the mesh bounding box (host)
+  double gx0 = 1e300, gy0 = 1e300, gx1 = -1e300, gy1 = -1e300;
+  for (int64_t i = 0; i < n_vert; ++i) {
+    gx0 = std::min(gx0, vxy[2 * i]);
+    gx1 = std::max(gx1, vxy[2 * i]);
+    gy0 = std::min(gy0, vxy[2 * i + 1]);
+    gy1 = std::max(gy1, vxy[2 * i + 1]);
+  }
+  const double W = gx1 - gx0, H = gy1 - gy0;
+  GridDev g;
+  g.cs = std::max(std::sqrt(std::max(W * H, 1e-300) / (double)n_tri) * 1.5, 1e-300);
+  while ((W / g.cs + 1) * (H / g.cs + 1) > double(1 << 24)) g.cs *= 1.5;
+  g.x0 = gx0 - 1e-9 * (W + H);
+  g.y0 = gy0 - 1e-9 * (W + H);
+  g.nx = std::max(1, (int)std::ceil((W + 2e-9 * (W + H)) / g.cs));
+  g.ny = std::max(1, (int)std::ceil((H + 2e-9 * (W + H)) / g.cs));
+  g.inv_cs = 1.0 / g.cs;
+  const int64_t ncell = (int64_t)g.nx * g.ny;
+  CUDA_TRY(c, cnt.ensure(sizeof(int64_t) * (n_tri + 1)));
+  CUDA_TRY(c, off.ensure(sizeof(int64_t) * (n_tri + 1)));
+  k_box_count<<<nblk(n_tri, 256), 256, 0, c->stream>>>(n_tri, dbb.as<double4>(), g, cnt.as<int64_t>());
+  CUDA_TRY(c, cudaMemsetAsync(cnt.as<int64_t>() + n_tri, 0, sizeof(int64_t), c->stream));
+  size_t tmpb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, cnt.as<int64_t>(), off.as<int64_t>(), n_tri + 1, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, cnt.as<int64_t>(), off.as<int64_t>(), n_tri + 1, c->stream);
+  int64_t np = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&np, off.as<int64_t>() + n_tri, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, keys.ensure(sizeof(int32_t) * (np + 1)));
+  CUDA_TRY(c, vals.ensure(sizeof(int32_t) * (np + 1)));
+  CUDA_TRY(c, keys2.ensure(sizeof(int32_t) * (np + 1)));
+  CUDA_TRY(c, cel.ensure(sizeof(int32_t) * (np + 1)));
+  CUDA_TRY(c, cb.ensure(sizeof(int64_t) * ncell));
+  CUDA_TRY(c, ce.ensure(sizeof(int64_t) * ncell));
+  k_box_fill<<<nblk(n_tri, 256), 256, 0, c->stream>>>(n_tri, dbb.as<double4>(), g, off.as<int64_t>(),
+                                                       keys.as<int32_t>(), vals.as<int32_t>());
+  int endbit = 1;
+  while ((1ll << endbit) < ncell) ++endbit;
+  tmpb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, keys.as<int32_t>(), keys2.as<int32_t>(), vals.as<int32_t>(),
+                                  cel.as<int32_t>(), (int)np, 0, endbit, c->stream);
+  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->d_tmp.p, tmpb, keys.as<int32_t>(), keys2.as<int32_t>(), vals.as<int32_t>(),
+                                  cel.as<int32_t>(), (int)np, 0, endbit, c->stream);
+  CUDA_TRY(c, cudaMemsetAsync(cb.p, 0, sizeof(int64_t) * ncell, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(ce.p, 0, sizeof(int64_t) * ncell, c->stream));
+  if (np > 0)
+    k_cell_ranges<<<nblk(np, 256), 256, 0, c->stream>>>(np, keys2.as<int32_t>(), cb.as<int64_t>(), ce.as<int64_t>());
+  VP_DISPATCH_P(p, launch_field_eval, c, n_pts, dp.as<double2>(), dtb.as<TriBox>(), dbb.as<double4>(), g,
+                cb.as<int64_t>(), ce.as<int64_t>(), cel.as<int32_t>(), dcf.as<double>(), dout.as<double>(),
+                deo.as<int32_t>());
+  CUDA_TRY(c, cudaGetLastError());
+  std::vector<int32_t> eo(n_pts);
+  CUDA_TRY(c, cudaMemcpyAsync(out, dout.p, sizeof(double) * n_pts, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(eo.data(), deo.p, sizeof(int32_t) * n_pts, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  int64_t nout = 0;
+  for (int64_t i = 0; i < n_pts; ++i) nout += eo[i] < 0;
+  if (elem_out) std::memcpy(elem_out, eo.data(), sizeof(int32_t) * n_pts);
+  if (n_outside) *n_outside = nout;
   return 0;
 }
 

@@ -314,3 +314,50 @@ def test_near_cache_depths_match_oracle(cfg2, depth):
     assert np.array_equal(lv, ref[:, 2].astype(np.int64))
     u_o, _, _ = O.evaluate(pr.txy[::97])
     assert rel(u, u_o) <= REL_TOL
+
+
+# ---------------------------------------------------------------------------
+# Potential interpolation: interp_coeffs + field_eval
+
+def test_interp_reproduces_polynomials_and_matches_numpy():
+    from oracle import binding as ob
+    vxy, tri = small_mesh()
+    p = 4
+    lx, ly = vp.lattice_nodes(p)
+    M = vp.koorn_size(p)
+    poly = lambda x, y: 0.3 + x - 2 * y + x * y ** 2 - 0.5 * x ** 4 + y ** 3 * x  # noqa: E731  degree 4
+    P = vxy[tri]
+    nodes = P[:, 0, None, :] + lx[None, :, None] * (P[:, 1] - P[:, 0])[:, None, :] + \
+        ly[None, :, None] * (P[:, 2] - P[:, 0])[:, None, :]
+    vals = poly(nodes[..., 0], nodes[..., 1])
+    with vp.Evaluator(0) as ev:
+        co, cond = ev.interp_coeffs(p, lx, ly, vals)
+        V = np.array([ob.koornwinder(p, x, y) for x, y in zip(lx, ly)])
+        ref = np.linalg.solve(V, vals.T).T
+        assert np.abs(co - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+        assert 1.0 <= cond < 1e6
+        rng = np.random.default_rng(3)
+        pts = rng.random((500, 2))
+        f, eo = ev.field_eval(vxy, tri, p, co, pts)
+        assert (eo >= 0).all()
+        assert np.abs(f - poly(pts[:, 0], pts[:, 1])).max() <= cond * 1e-13
+        f2, eo2 = ev.field_eval(vxy, tri, p, co, np.array([[2.0, 2.0], [0.5, 0.25]]), allow_outside=True)
+        assert eo2[0] == -1 and np.isnan(f2[0]) and eo2[1] == 0
+        with pytest.raises(vp.NumericalError):
+            ev.field_eval(vxy, tri, p, co, np.array([[2.0, 2.0]]))
+
+
+def test_potential_field_of_config1(cfg1):
+    """evaluate_field phase 3: u at the interpolation nodes -> PotentialField ->
+    field_eval reproduces the nodal values and approximates u elsewhere."""
+    pr, ev, O = cfg1
+    u, _ = ev.evaluate(pr.txy)
+    lx, ly = vp.lattice_nodes(pr.p)
+    co, cond = ev.interp_coeffs(pr.p, lx, ly, u.reshape(pr.n_tri, -1))
+    f, eo = ev.field_eval(pr.vxy, pr.tri, pr.p, co, pr.txy)
+    assert np.abs(f - u).max() <= cond * 1e-13 * np.abs(u).max()
+    rng = np.random.default_rng(5)
+    pts = 0.05 + 0.9 * rng.random((64, 2))
+    fi, _ = ev.field_eval(pr.vxy, pr.tri, pr.p, co, pts)
+    u_o, _, _ = O.evaluate(pts)
+    assert np.abs(fi - u_o).max() <= 1e-5 * np.abs(u_o).max()
