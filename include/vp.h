@@ -151,6 +151,13 @@ int vp_field_eval(vp_ctx* ctx, int64_t n_vert, const double* vxy, int64_t n_tri,
                   int p, const double* coeffs, int64_t n_pts, const double* pts, double* out,
                   int32_t* elem_out, int64_t* n_outside);
 
+/* Near-field model: 0 = precise three-Bernstein-ellipse model (SPEC.md:
+ * 411-458, default), 1 = the naive ball baseline (circumscribed circle scaled
+ * by ball_factor, 1.5 in SPEC.md:585) for both the lists and the near_eval
+ * sub-simplex acceptance (depth capped at 20).  Used for the paper's
+ * correction-count comparison (Table near_corr). */
+int vp_set_near_model(vp_ctx* ctx, int model, double ball_factor);
+
 /* Near-leaf density cache: w_i f at the N_n-rule nodes of every sub-simplex
  * of depth <= max_depth (-1 disables; default 3) is precomputed per element
  * and shared by all targets, within max_bytes of HBM (0 -> 12 GiB; the depth

@@ -35,6 +35,7 @@ class VpoProblem(ctypes.Structure):
         ("n_l", ctypes.c_int), ("gl_x", _d_p), ("gl_w", _d_p),
         ("n_g", ctypes.c_int), ("ggq_r", _d_p), ("ggq_w", _d_p),
         ("eps", ctypes.c_double),
+        ("near_model", ctypes.c_int), ("pad_", ctypes.c_int), ("ball_factor", ctypes.c_double),
     ]
 
 
@@ -113,7 +114,7 @@ def _check(rc):
 class Oracle:
     """Holds the arrays of one problem and exposes the oracle entry points."""
 
-    def __init__(self, vxy, tri, p, coeffs, rules):
+    def __init__(self, vxy, tri, p, coeffs, rules, near_model=0, ball_factor=1.5):
         self.vxy = np.ascontiguousarray(vxy, dtype=np.float64).reshape(-1, 2)
         self.tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
         self.coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
@@ -128,11 +129,12 @@ class Oracle:
             q=rules.q, len_q=len(k[0]), far_x=_d(k[0]), far_y=_d(k[1]), far_w=_d(k[2]),
             n_n=rules.n_n, len_n=len(k[3]), near_x=_d(k[3]), near_y=_d(k[4]), near_w=_d(k[5]),
             n_l=len(k[6]), gl_x=_d(k[6]), gl_w=_d(k[7]),
-            n_g=rules.n_g, ggq_r=_d(k[8]), ggq_w=_d(k[9]), eps=rules.eps)
+            n_g=rules.n_g, ggq_r=_d(k[8]), ggq_w=_d(k[9]), eps=rules.eps,
+            near_model=near_model, ball_factor=ball_factor)
 
     @classmethod
-    def from_problem(cls, pr):
-        return cls(pr.vxy, pr.tri, pr.p, pr.coeffs, pr.rules)
+    def from_problem(cls, pr, near_model=0, ball_factor=1.5):
+        return cls(pr.vxy, pr.tri, pr.p, pr.coeffs, pr.rules, near_model, ball_factor)
 
     def nearlist(self, txy):
         t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)

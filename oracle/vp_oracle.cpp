@@ -133,6 +133,32 @@ double w_edge(int len, const double* x, const double* y, const double* w) {
   return best;
 }
 
+// Ball near-field model: circumscribed circle scaled by
+// `factor`, centre stored relative to vertex a; exact operation order shared
+// with the GPU (vp_device.cuh rn_ball).
+struct Ball {
+  double ux, uy, rr;  // centre - a, factor^2 * R^2
+};
+Ball ball_of(double ax, double ay, double bx, double by, double cx, double cy, double factor) {
+  const double bxr = bx - ax, byr = by - ay, cxr = cx - ax, cyr = cy - ay;
+  const double t1 = bxr * cyr, t2 = byr * cxr;
+  const double d = 2.0 * (t1 - t2);
+  const double b2 = bxr * bxr + byr * byr, c2 = cxr * cxr + cyr * cyr;
+  const double u1 = cyr * b2, u2 = byr * c2;
+  const double v1 = bxr * c2, v2 = cxr * b2;
+  Ball B;
+  B.ux = (u1 - u2) / d;
+  B.uy = (v1 - v2) / d;
+  const double R2 = B.ux * B.ux + B.uy * B.uy;
+  B.rr = (factor * factor) * R2;
+  return B;
+}
+bool in_ball(const Ball& B, double ax, double ay, double tx, double ty) {
+  const double dx = (tx - ax) - B.ux, dy = (ty - ay) - B.uy;
+  return dx * dx + dy * dy < B.rr;
+}
+constexpr int kBallMaxDepth = 20;  // ball model: accept at this depth (no rho_d cut-off exists)
+
 // ---------------------------------------------------------------------------
 // Quadtree over points (quadtree.hpp:24-126): closed rectangles, quadrant by
 // >= against the centre, leaf capacity m, minimum box diameter 1e-12 * root.
@@ -289,6 +315,16 @@ struct Setup {
         const int32_t id[3] = {p->tri[3 * e], p->tri[3 * e + 1], p->tri[3 * e + 2]};
         double px[3], py[3];
         for (int k = 0; k < 3; ++k) { px[k] = p->vxy[2 * id[k]]; py[k] = p->vxy[2 * id[k] + 1]; }
+        if (p->near_model == 1) {  // ball model: ta = (ux, uy, factor^2 R^2)
+          const Ball B = ball_of(px[0], py[0], px[1], py[1], px[2], py[2], p->ball_factor);
+          two_a[3 * e] = B.ux;
+          two_a[3 * e + 1] = B.uy;
+          two_a[3 * e + 2] = B.rr;
+          const double r = std::sqrt(B.rr) * (1.0 + 1e-9) + 1e-300;
+          const double cxm = px[0] + B.ux, cym = py[0] + B.uy;
+          bb[4 * e] = cxm - r; bb[4 * e + 1] = cym - r; bb[4 * e + 2] = cxm + r; bb[4 * e + 3] = cym + r;
+          continue;
+        }
         if (!(rho0[e] > 1.0)) {  // model undefined -> element all-near
           all_near[e] = 1;
           all_near_ids.push_back((int32_t)e);
@@ -360,6 +396,10 @@ struct Setup {
   // t strictly inside the union of the three open ellipses of e
   // (SPEC.md:450-458): |t-P| + |t-Q| < 2a for side PQ.
   bool in_near(int64_t e, double tx, double ty) const {
+    if (pr->near_model == 1) {
+      const Ball B{two_a[3 * e], two_a[3 * e + 1], two_a[3 * e + 2]};
+      return in_ball(B, pr->vxy[2 * pr->tri[3 * e]], pr->vxy[2 * pr->tri[3 * e] + 1], tx, ty);
+    }
     if (all_near[e]) return true;
     const int32_t* id = pr->tri + 3 * e;
     double d[3];
@@ -446,7 +486,10 @@ struct Setup {
     }
     const double rd = rho0n[e] * kd[d];
     bool accept;
-    if (!(rd > 1.0)) {
+    if (pr->near_model == 1) {
+      const Ball B = ball_of(px[0], py[0], px[1], py[1], px[2], py[2], pr->ball_factor);
+      accept = d >= kBallMaxDepth || !in_ball(B, px[0], py[0], tx, ty);
+    } else if (!(rd > 1.0)) {
       accept = true;
       acc.rho_le1++;
     } else {

@@ -46,6 +46,9 @@ typedef struct {
   const double* ggq_r;
   const double* ggq_w;
   double eps;
+  int near_model;      /* 0 precise (Bernstein ellipses), 1 ball */
+  int pad_;
+  double ball_factor;  /* ball = circumscribed circle scaled by this (1.5) */
 } vpo_problem;
 
 typedef struct {

@@ -85,6 +85,7 @@ _SIGS = [
     ("vp_field_eval", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, ctypes.c_int64, c_int32_p,
                                      ctypes.c_int, c_double_p, ctypes.c_int64, c_double_p, c_double_p, c_int32_p,
                                      c_int64_p]),
+    ("vp_set_near_model", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
     ("vp_set_near_cache", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     ("vp_set_far_method", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("vp_device_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),

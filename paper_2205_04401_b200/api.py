@@ -293,6 +293,11 @@ class Evaluator:
         m = {"direct": 0, "fmm": 1}[method]
         _check(self._L.vp_set_far_method(self._h, m, order, leaf_size), self._err())
 
+    def set_near_model(self, model: str = "precise", ball_factor: float = 1.5):
+        """'precise' (Bernstein ellipses, default) or 'ball' (SPEC.md:585 baseline)."""
+        m = {"precise": 0, "ball": 1}[model]
+        _check(self._L.vp_set_near_model(self._h, m, ball_factor), self._err())
+
     def set_near_cache(self, max_depth: int = 3, max_bytes: int = 0):
         """Per-element cache of near-rule densities for sub-simplices of depth
         <= max_depth (-1 disables)."""

@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kMaxPdev = 12;
 constexpr int kMaxModes = (kMaxPdev + 1) * (kMaxPdev + 2) / 2;  // 91
-constexpr int kMaxFar = 512;
+constexpr int kMaxFar = 1024;
 constexpr int kMaxNearRule = 256;
 constexpr int kMaxGL = 64;
 constexpr int kMaxGGQ = 32;
@@ -40,6 +40,8 @@ __constant__ double c_cn[kMaxModes];  // Koornwinder normalisation c_mn by index
 
 struct RulesDev {
   int len_q, len_n, n_l, n_g1, n_n, q;
+  int near_model, pad_;   // 0 precise, 1 ball
+  double ball_factor;
   double far_x[kMaxFar], far_y[kMaxFar], far_w[kMaxFar];
   double near_x[kMaxNearRule], near_y[kMaxNearRule], near_w[kMaxNearRule];
   double gl_x[kMaxGL], gl_w[kMaxGL];
@@ -88,7 +90,7 @@ __global__ void k_bin_count(int64_t E, const ElemRec* __restrict__ el, GridDev g
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const ElemRec& T = el[e];
-  if (T.ta0 < 0.0) {
+  if (T.ball == 0.0 && T.ta0 < 0.0) {  // all-near: scanned by every target instead
     cnt[e] = 0;
     return;
   }
@@ -103,7 +105,7 @@ __global__ void k_bin_fill(int64_t E, const ElemRec* __restrict__ el, GridDev g,
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const ElemRec& T = el[e];
-  if (T.ta0 < 0.0) return;
+  if (T.ball == 0.0 && T.ta0 < 0.0) return;
   const int cx0 = cell_coord(T.bx0, g.x0, g.inv_cs, g.nx), cx1 = cell_coord(T.bx1, g.x0, g.inv_cs, g.nx);
   const int cy0 = cell_coord(T.by0, g.y0, g.inv_cs, g.ny), cy1 = cell_coord(T.by1, g.y0, g.inv_cs, g.ny);
   int64_t o = off[e];
@@ -165,7 +167,7 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
       ++ia;
     }
     const ElemRec& R = el[id];
-    if (R.ta0 >= 0.0 && !(tx >= R.bx0 && tx <= R.bx1 && ty >= R.by0 && ty <= R.by1)) continue;
+    if ((R.ball != 0.0 || R.ta0 >= 0.0) && !(tx >= R.bx0 && tx <= R.bx1 && ty >= R.by0 && ty <= R.by1)) continue;
     if (self < 0) {
       double xi, eta;
       if (rn_locate(R, tx, ty, xi, eta)) {
@@ -331,10 +333,23 @@ __device__ __forceinline__ void decode_path(unsigned long long path, int d, doub
 
 // acceptance test of one sub-simplex (same operation order as the oracle's
 // near_rec): rho_d = rho0n 4^{-d/N_n}; rho_d <= 1 accepts.
+constexpr int kBallMaxDepth = 20;  // ball model: accept at this depth (oracle: same)
+
 __device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double ty, double rd,
                                             double ax, double ay, double bx, double by, double cx,
-                                            double cy, bool& rle1) {
+                                            double cy, bool& rle1, int d, double ball_factor) {
   rle1 = false;
+  if (ball_factor > 0.0) {
+    if (d >= kBallMaxDepth) return true;
+    const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
+    double px[3], py[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      px[k] = rn_add(E.x0, rn_add(rn_mul(vxs[k], E.e1x), rn_mul(vys[k], E.e2x)));
+      py[k] = rn_add(E.y0, rn_add(rn_mul(vxs[k], E.e1y), rn_mul(vys[k], E.e2y)));
+    }
+    return !rn_ball_test(px[0], py[0], px[1], py[1], px[2], py[2], ball_factor, tx, ty);
+  }
   if (!(rd > 1.0)) {
     rle1 = true;
     return true;
@@ -368,6 +383,7 @@ __global__ void __launch_bounds__(128)
   __shared__ double skd[kMaxNearDepth + 2];
   for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
+  const double ball_factor = R->near_model == 1 ? R->ball_factor : 0.0;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rle1 = 0;
   int maxd = 0;
@@ -387,7 +403,7 @@ __global__ void __launch_bounds__(128)
       double ax, ay, bx, by, cx, cy;
       decode_path(path, d, ax, ay, bx, by, cx, cy);
       bool le1;
-      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1)) {
+      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor)) {
         if (FILL) leaves[o++] = code;
         ++n;
         rle1 += le1 ? 1ull : 0ull;
@@ -1060,6 +1076,8 @@ struct vp_ctx {
   DevBuf d_selftab;
   int selftab_p = -1;
   // near-leaf density cache (depth <= cache_depth sub-simplices), see k_near_cache
+  int near_model = 0;
+  double ball_factor = 1.5;
   int cache_max_depth = 3, cache_depth = -1;
   int64_t cache_max_bytes = 12ll << 30;
   DevBuf d_cacheV, d_gcache;
@@ -1127,6 +1145,25 @@ int build_elements(vp_ctx* c) {
     const double wnn = wn * R.det;
     const double denn = r.eps * cnn;
     R.rho0n = std::pow(wnn / denn, 1.0 / (double)r.n_n);
+    if (c->near_model == 1) {  // ball model, same operations as the oracle's ball_of
+      const double bxr = px[1] - px[0], byr = py[1] - py[0], cxr = px[2] - px[0], cyr = py[2] - py[0];
+      const double t1 = bxr * cyr, t2 = byr * cxr;
+      const double d = 2.0 * (t1 - t2);
+      const double b2 = bxr * bxr + byr * byr, c2 = cxr * cxr + cyr * cyr;
+      const double u1 = cyr * b2, u2 = byr * c2, v1 = bxr * c2, v2 = cxr * b2;
+      R.ta0 = (u1 - u2) / d;
+      R.ta1 = (v1 - v2) / d;
+      const double R2 = R.ta0 * R.ta0 + R.ta1 * R.ta1;
+      R.ta2 = (c->ball_factor * c->ball_factor) * R2;
+      R.ball = 1.0;
+      const double rr = std::sqrt(R.ta2) * (1.0 + 1e-9) + 1e-300;
+      const double cxm = px[0] + R.ta0, cym = py[0] + R.ta1;
+      R.bx0 = cxm - rr; R.by0 = cym - rr; R.bx1 = cxm + rr; R.by1 = cym + rr;
+      gx0 = std::min(gx0, R.bx0); gy0 = std::min(gy0, R.by0);
+      gx1 = std::max(gx1, R.bx1); gy1 = std::max(gy1, R.by1);
+      ext.push_back(std::max(R.bx1 - R.bx0, R.by1 - R.by0));
+      continue;
+    }
     if (!(rho0 > 1.0)) {  // SPEC.md:444 all-near
       R.ta0 = R.ta1 = R.ta2 = -1.0;
       c->h_allnear.push_back((int32_t)e);
@@ -1745,6 +1782,24 @@ void vp_destroy(vp_ctx* c) {
   delete c;
 }
 
+int vp_set_near_model(vp_ctx* c, int model, double ball_factor) {
+  if (!c) return 1;
+  if (model != 0 && model != 1) return set_err(c, 1, "set_near_model: model must be 0 (precise) or 1 (ball)");
+  if (model == 1 && !(ball_factor >= 1.0)) return set_err(c, 1, "set_near_model: ball factor must be >= 1");
+  c->near_model = model;
+  c->ball_factor = model == 1 ? ball_factor : 1.5;
+  if (c->have_rules) {
+    c->h_rd.near_model = c->near_model;
+    c->h_rd.ball_factor = c->ball_factor;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_rules.p, &c->h_rd, sizeof(RulesDev), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->have_mesh)
+      if (int rc = build_elements(c)) return rc;
+  }
+  return 0;
+}
+
 int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
   if (!c) return 1;
   if (max_depth < -1 || max_depth > 6) return set_err(c, 1, "set_near_cache: max_depth must be in [-1, 6]");
@@ -1822,7 +1877,7 @@ int vp_set_rules(vp_ctx* c, const vp_rules* r) {
   if (!c) return 1;
   if (!r) return set_err(c, 1, "set_rules: null rules");
   if (r->len_q <= 0 || r->len_q > kMaxFar || !r->far_x || !r->far_y || !r->far_w)
-    return set_err(c, 1, "set_rules: far rule length must be in [1, 512]");
+    return set_err(c, 1, "set_rules: far rule length must be in [1, 1024]");
   if (r->len_n <= 0 || r->len_n > kMaxNearRule || !r->near_x || !r->near_y || !r->near_w)
     return set_err(c, 1, "set_rules: near rule length must be in [1, 256]");
   if (r->n_l <= 0 || r->n_l > kMaxGL || !r->gl_x || !r->gl_w)
@@ -1854,6 +1909,8 @@ int vp_set_rules(vp_ctx* c, const vp_rules* r) {
   RulesDev& d = c->h_rd;
   std::memset(&d, 0, sizeof(d));
   d.len_q = r->len_q; d.len_n = r->len_n; d.n_l = r->n_l; d.n_g1 = r->n_g + 1; d.n_n = r->n_n; d.q = r->q;
+  d.near_model = c->near_model;
+  d.ball_factor = c->ball_factor;
   for (int i = 0; i < r->len_q; ++i) { d.far_x[i] = r->far_x[i]; d.far_y[i] = r->far_y[i]; d.far_w[i] = r->far_w[i]; }
   for (int i = 0; i < r->len_n; ++i) { d.near_x[i] = r->near_x[i]; d.near_y[i] = r->near_y[i]; d.near_w[i] = r->near_w[i]; }
   for (int i = 0; i < r->n_l; ++i) { d.gl_x[i] = r->gl_x[i]; d.gl_w[i] = r->gl_w[i]; }

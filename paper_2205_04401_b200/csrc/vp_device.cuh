@@ -23,7 +23,7 @@ struct alignas(64) ElemRec {
   double e1x, e1y, e2x, e2y, det; // affine map, det = |J| = 2 area
   double rho0n;                   // rho0 of the N_n (near-rule) model
   double bx0, by0, bx1, by1;      // near-field bbox (conservative)
-  double pad;
+  double ball;                    // != 0: ball model, ta0/ta1 = centre - v0, ta2 = factor^2 R^2
 };
 static_assert(sizeof(ElemRec) == 192, "ElemRec layout");
 
@@ -57,8 +57,27 @@ __device__ __forceinline__ bool rn_locate(const ElemRec& E, double tx, double ty
   return xi >= -kBaryTol && eta >= -kBaryTol && l0 >= -kBaryTol;
 }
 
-// t inside the union of the element's three open ellipses
+// Ball near-field model: circumscribed circle of (a, b, c)
+// scaled by `factor`; same operation order as the oracle's ball_of/in_ball.
+__device__ __forceinline__ bool rn_ball_test(double ax, double ay, double bx, double by, double cx, double cy,
+                                             double factor, double tx, double ty) {
+  const double bxr = rn_sub(bx, ax), byr = rn_sub(by, ay), cxr = rn_sub(cx, ax), cyr = rn_sub(cy, ay);
+  const double d = rn_mul(2.0, rn_sub(rn_mul(bxr, cyr), rn_mul(byr, cxr)));
+  const double b2 = rn_add(rn_mul(bxr, bxr), rn_mul(byr, byr)), c2 = rn_add(rn_mul(cxr, cxr), rn_mul(cyr, cyr));
+  const double ux = rn_div(rn_sub(rn_mul(cyr, b2), rn_mul(byr, c2)), d);
+  const double uy = rn_div(rn_sub(rn_mul(bxr, c2), rn_mul(cxr, b2)), d);
+  const double rr = rn_mul(rn_mul(factor, factor), rn_add(rn_mul(ux, ux), rn_mul(uy, uy)));
+  const double dx = rn_sub(rn_sub(tx, ax), ux), dy = rn_sub(rn_sub(ty, ay), uy);
+  return rn_add(rn_mul(dx, dx), rn_mul(dy, dy)) < rr;
+}
+
+// t inside the union of the element's three open ellipses,
+// or inside its ball for the ball model
 __device__ __forceinline__ bool rn_in_near(const ElemRec& E, double tx, double ty) {
+  if (E.ball != 0.0) {
+    const double dx = rn_sub(rn_sub(tx, E.x0), E.ta0), dy = rn_sub(rn_sub(ty, E.y0), E.ta1);
+    return rn_add(rn_mul(dx, dx), rn_mul(dy, dy)) < E.ta2;
+  }
   if (E.ta0 < 0.0) return true;  // all-near model
   const double d0 = rn_dist(tx, ty, E.x0, E.y0);
   const double d1 = rn_dist(tx, ty, E.x1, E.y1);

@@ -361,3 +361,21 @@ def test_potential_field_of_config1(cfg1):
     fi, _ = ev.field_eval(pr.vxy, pr.tri, pr.p, co, pts)
     u_o, _, _ = O.evaluate(pts)
     assert np.abs(fi - u_o).max() <= 1e-5 * np.abs(u_o).max()
+
+
+# ---------------------------------------------------------------------------
+# Ball near-field baseline
+
+@pytest.mark.parametrize("cfg,stride", [(1, 3), (2, 61)])
+def test_ball_model_lists_and_u_match_oracle(cfg, stride):
+    pr = vp.load_config(cfg)
+    O = Oracle.from_problem(pr, near_model=1, ball_factor=1.5)
+    sub = pr.txy[::stride]
+    with vp.Evaluator(0) as ev:
+        ev.load(pr)
+        ev.set_near_model("ball", 1.5)
+        assert_lists_equal(ev, O, pr.txy)
+        u_g, st = ev.evaluate(sub)
+    u_o, _, sto = O.evaluate(sub)
+    assert rel(u_g, u_o) <= REL_TOL
+    assert st["n_leaves"] == sto["n_leaves"] and st["n_near_pairs"] == sto["n_near_pairs"]

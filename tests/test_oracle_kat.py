@@ -197,3 +197,26 @@ def test_empty_target_array(cfg1):
     assert len(s) == 0 and list(off) == [0] and len(ids) == 0
     u, _, st = O.evaluate(np.zeros((0, 2)))
     assert len(u) == 0
+
+
+def test_ball_model_lists_match_brute_force_and_is_coarser_on_the_disk():
+    """Ball baseline: lists equal a brute-force scan, and on the
+    disk the precise model needs fewer corrections (PAPER.md Table near_corr)."""
+    pr = vp.load_config(2)
+    sub = pr.txy[::509]
+    Ob = Oracle.from_problem(pr, near_model=1)
+    s, off, ids = Ob.nearlist(sub)
+    P = pr.vxy[pr.tri]
+    a, b, c = P[:, 0], P[:, 1], P[:, 2]
+    bxr, byr, cxr, cyr = b[:, 0] - a[:, 0], b[:, 1] - a[:, 1], c[:, 0] - a[:, 0], c[:, 1] - a[:, 1]
+    d = 2.0 * (bxr * cyr - byr * cxr)
+    b2, c2 = bxr * bxr + byr * byr, cxr * cxr + cyr * cyr
+    ux, uy = (cyr * b2 - byr * c2) / d, (bxr * c2 - cxr * b2) / d
+    rr = 2.25 * (ux * ux + uy * uy)
+    for k, t in enumerate(sub):
+        dx, dy = (t[0] - a[:, 0]) - ux, (t[1] - a[:, 1]) - uy
+        near = set(np.nonzero(dx * dx + dy * dy < rr)[0]) - {s[k]}
+        assert sorted(near) == list(ids[off[k]:off[k + 1]])
+    _, _, stb = Ob.evaluate(sub)
+    _, _, stp = Oracle.from_problem(pr).evaluate(sub)
+    assert stp["n_near_pairs"] < stb["n_near_pairs"] and stp["n_leaves"] < stb["n_leaves"]
