@@ -379,3 +379,33 @@ def test_ball_model_lists_and_u_match_oracle(cfg, stride):
     u_o, _, sto = O.evaluate(sub)
     assert rel(u_g, u_o) <= REL_TOL
     assert st["n_leaves"] == sto["n_leaves"] and st["n_near_pairs"] == sto["n_near_pairs"]
+
+
+@pytest.mark.parametrize("q", [10, 24])
+def test_config5_q_sweep_sample(q):
+    """Config 5 (262k-triangle graded star) at the sweep's extreme far orders."""
+    pr = vp.load_config(5, q)
+    O = Oracle.from_problem(pr)
+    sub = pr.txy[::200003]
+    with vp.Evaluator(0) as ev:
+        ev.load(pr)
+        assert_lists_equal(ev, O, pr.txy[::40009])
+        u_g, st = ev.evaluate(sub)
+    u_o, _, sto = O.evaluate(sub)
+    assert rel(u_g, u_o) <= REL_TOL
+    assert st["n_leaves"] == sto["n_leaves"] and st["n_panels"] == sto["n_panels"]
+
+
+def test_p12_on_config1_mesh():
+    pr = vp.load_config(1)
+    co = vp.project_density(pr.vxy, pr.tri, 12, vp.F_SQUARE)
+    r = vp.make_rules(14)
+    O = Oracle(pr.vxy, pr.tri, 12, co, r)
+    sub = pr.txy[::11]
+    with vp.Evaluator(0) as ev:
+        ev.set_mesh(pr.vxy, pr.tri)
+        ev.set_rules(r)
+        ev.set_density(12, co)
+        u_g, _ = ev.evaluate(sub)
+    u_o, _, _ = O.evaluate(sub)
+    assert rel(u_g, u_o) <= REL_TOL
