@@ -468,6 +468,24 @@ struct Setup {
     int32_t max_depth = 0;
     int err = 0;
   };
+  // side lengths of the depth-0 image of the reference simplex (vertices
+  // x0 + (xi e1 + eta e2), the sub-simplex vertex formula at depth 0)
+  void side_lengths0(int64_t e, double l[3]) const {
+    const double rx[3] = {0.0, 1.0, 0.0}, ry[3] = {0.0, 0.0, 1.0};
+    double px[3], py[3];
+    for (int k = 0; k < 3; ++k) {
+      const double s0 = rx[k] * e1x[e], s1 = ry[k] * e2x[e];
+      px[k] = x0[e] + (s0 + s1);
+      const double t0 = rx[k] * e1y[e], t1 = ry[k] * e2y[e];
+      py[k] = y0[e] + (t0 + t1);
+    }
+    for (int k = 0; k < 3; ++k) {
+      const int k1 = (k + 1) % 3;
+      const double dx = px[k1] - px[k], dy = py[k1] - py[k];
+      l[k] = std::sqrt(dx * dx + dy * dy);
+    }
+  }
+
   void near_rec(int64_t e, double tx, double ty, const double a[2], const double b[2],
                 const double c[2], int d, NearAcc& acc) const {
     if (d > kMaxNearDepth) {
@@ -499,12 +517,16 @@ struct Setup {
         const double dx = tx - px[k], dy = ty - py[k];
         dist[k] = std::sqrt(dx * dx + dy * dy);
       }
+      // the midpoint split makes every depth-d sub-simplex congruent to the
+      // element scaled by 2^-d with the same side order, so its side k has
+      // length l_k 2^-d exactly (l_k of the depth-0 reference image)
+      double l0[3];
+      side_lengths0(e, l0);
+      const double sc = std::ldexp(1.0, -d);
       bool nearp = false;
       for (int k = 0; k < 3 && !nearp; ++k) {
         const int k1 = (k + 1) % 3;
-        const double sxk = px[k1] - px[k], syk = py[k1] - py[k];
-        const double len = std::sqrt(sxk * sxk + syk * syk);
-        const double ta = g * len;
+        const double ta = g * (l0[k] * sc);
         if (dist[k] + dist[k1] < ta) nearp = true;
       }
       accept = !nearp;

@@ -337,7 +337,8 @@ constexpr int kBallMaxDepth = 20;  // ball model: accept at this depth (oracle: 
 
 __device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double ty, double rd,
                                             double ax, double ay, double bx, double by, double cx,
-                                            double cy, bool& rle1, int d, double ball_factor) {
+                                            double cy, bool& rle1, int d, double ball_factor,
+                                            const double l0[3]) {
   rle1 = false;
   if (ball_factor > 0.0) {
     if (d >= kBallMaxDepth) return true;
@@ -356,20 +357,38 @@ __device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double 
   }
   const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
   const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
-  double px[3], py[3], dist[3];
+  double dist[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    px[k] = rn_add(E.x0, rn_add(rn_mul(vxs[k], E.e1x), rn_mul(vys[k], E.e2x)));
-    py[k] = rn_add(E.y0, rn_add(rn_mul(vxs[k], E.e1y), rn_mul(vys[k], E.e2y)));
-    dist[k] = rn_dist(tx, ty, px[k], py[k]);
+    const double px = rn_add(E.x0, rn_add(rn_mul(vxs[k], E.e1x), rn_mul(vys[k], E.e2x)));
+    const double py = rn_add(E.y0, rn_add(rn_mul(vxs[k], E.e1y), rn_mul(vys[k], E.e2y)));
+    dist[k] = rn_dist(tx, ty, px, py);
+  }
+  // every depth-d sub-simplex is the element's depth-0 image scaled by 2^-d
+  // with the same side order: side k has length l0[k] 2^-d exactly
+  const double sc = ldexp(1.0, -d);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int k1 = (k + 1) % 3;
+    if (rn_add(dist[k], dist[k1]) < rn_mul(g, rn_mul(l0[k], sc))) return false;
+  }
+  return true;
+}
+
+// side lengths of the depth-0 image of the reference simplex (oracle's side_lengths0)
+__device__ __forceinline__ void side_lengths0(const ElemRec& E, double l0[3]) {
+  const double rx[3] = {0.0, 1.0, 0.0}, ry[3] = {0.0, 0.0, 1.0};
+  double px[3], py[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    px[k] = rn_add(E.x0, rn_add(rn_mul(rx[k], E.e1x), rn_mul(ry[k], E.e2x)));
+    py[k] = rn_add(E.y0, rn_add(rn_mul(rx[k], E.e1y), rn_mul(ry[k], E.e2y)));
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int k1 = (k + 1) % 3;
-    const double len = rn_dist(px[k1], py[k1], px[k], py[k]);
-    if (rn_add(dist[k], dist[k1]) < rn_mul(g, len)) return false;
+    l0[k] = rn_dist(px[k1], py[k1], px[k], py[k]);
   }
-  return true;
 }
 
 template <bool FILL>
@@ -391,6 +410,8 @@ __global__ void __launch_bounds__(128)
     const int32_t e = pair_elem[p];
     const double2 tp = txy[pair_tgt[p]];
     const ElemRec E = el[e];
+    double l0[3];
+    side_lengths0(E, l0);
     unsigned long long stack[kStackCap];
     int sp = 0;
     stack[sp++] = 0ull;
@@ -403,7 +424,7 @@ __global__ void __launch_bounds__(128)
       double ax, ay, bx, by, cx, cy;
       decode_path(path, d, ax, ay, bx, by, cx, cy);
       bool le1;
-      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor)) {
+      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0)) {
         if (FILL) leaves[o++] = code;
         ++n;
         rle1 += le1 ? 1ull : 0ull;
@@ -493,17 +514,23 @@ __device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __
   return acc;
 }
 
-template <int P>
-__global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
+// K4b in two specialisations so each runs at its own occupancy:
+//   MODE 0: leaves at depth <= cache_depth (weighted densities read from the
+//           per-element cache; ~25 FP64 ops per node) + the element's point
+//           sum; writes part_a[p] and part_s[p];
+//   MODE 1: deeper leaves (Koornwinder recurrence at every node); writes part_b[p].
+// k_near_combine forms corr[p] = part_a + part_b - part_s in fixed order.
+template <int P, int MODE>
+__global__ void __launch_bounds__(NEAR_WARPS * 32, MODE == 0 ? 4 : VP_NEAR_MINB)
     k_near_int(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
                const double2* __restrict__ txy, const ElemRec* __restrict__ el,
                const double* __restrict__ coeffs, const int64_t* __restrict__ loff,
                const unsigned long long* __restrict__ leaves, const double* __restrict__ sx,
                const double* __restrict__ sy, const double* __restrict__ sq,
                const RulesDev* __restrict__ R, const double* __restrict__ gcache, int cache_depth,
-               double* __restrict__ corr, double* __restrict__ sub_out) {
+               double* __restrict__ part, double* __restrict__ part_s, bool exact_zero) {
   constexpr int M = (P + 1) * (P + 2) / 2;
-  __shared__ double scc[NEAR_WARPS][M];
+  __shared__ double scc[MODE == 1 ? NEAR_WARPS : 1][M];
   __shared__ double2 sga[NEAR_WARPS][32], sgb[NEAR_WARPS][32], sgc[NEAR_WARPS][32];
   __shared__ double sgs[NEAR_WARPS][32];
   __shared__ int sslot[NEAR_WARPS][32];
@@ -518,7 +545,8 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* cc = scc[wid];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
   for (int64_t p = (int64_t)blockIdx.x * NEAR_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * NEAR_WARPS) {
     const int32_t t = pair_tgt[p], e = pair_elem[p];
     const double2 tp = txy[t];
@@ -526,45 +554,43 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
     const ElemRec& Er = el[e];
     const double X0 = Er.x0, Y0 = Er.y0, E1x = Er.e1x, E1y = Er.e1y, E2x = Er.e2x, E2y = Er.e2y;
     const double det = Er.det;
-    for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
     const int64_t l0 = loff[p], nl = loff[p + 1] - l0;
-    const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
     const double* gce = gcache + (int64_t)e * nslot * Ln;
-    const unsigned lt_mask = (1u << lane) - 1u;
     double acc = 0.0;
+    bool coeffs_loaded = false;
     for (int64_t lb = 0; lb < nl; lb += 32) {
       const int nb = (int)min((int64_t)32, nl - lb);
       __syncwarp();
-      // decode the batch; leaves at depth <= cache_depth go first (their
-      // weighted densities w_i f are read from the per-element cache)
-      bool cached = false;
-      int pos = 0, nc = 0;
-      {
-        unsigned long long code = 0;
-        int d = 0;
-        if (lane < nb) {
-          code = leaves[l0 + lb + lane];
-          d = (int)(code >> 58);
-          cached = d <= cache_depth;
-        }
-        const unsigned cm = __ballot_sync(0xffffffffu, lane < nb && cached);
-        nc = __popc(cm);
-        pos = cached ? __popc(cm & lt_mask) : nc + (lane - __popc(cm & lt_mask));
-        if (lane < nb) {
-          double ax, ay, bx, by, cx, cy;
-          const unsigned long long path = code & kPathMask;
-          decode_path(path, d, ax, ay, bx, by, cx, cy);
-          sga[wid][pos] = make_double2(ax, ay);
-          sgb[wid][pos] = make_double2(bx - ax, by - ay);
-          sgc[wid][pos] = make_double2(cx - ax, cy - ay);
-          sgs[wid][pos] = det * ldexp(1.0, -2 * d) * kInv4Pi;
-          sslot[wid][pos] = cached ? (((1 << (2 * d)) - 1) / 3 + (int)path) : -1;
-        }
+      // this mode's leaves of the batch, compacted to the front
+      unsigned long long code = 0;
+      int d = 0;
+      bool mine = false;
+      if (lane < nb) {
+        code = leaves[l0 + lb + lane];
+        d = (int)(code >> 58);
+        mine = MODE == 0 ? d <= cache_depth : d > cache_depth;
+      }
+      const unsigned mm = __ballot_sync(0xffffffffu, mine);
+      const int nm = __popc(mm);
+      if (nm == 0) continue;
+      if (MODE == 1 && !coeffs_loaded) {
+        for (int j = lane; j < M; j += 32) scc[MODE == 1 ? wid : 0][j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+        coeffs_loaded = true;
+      }
+      if (mine) {
+        const int pos = __popc(mm & lt_mask);
+        double ax, ay, bx, by, cx, cy;
+        const unsigned long long path = code & kPathMask;
+        decode_path(path, d, ax, ay, bx, by, cx, cy);
+        sga[wid][pos] = make_double2(ax, ay);
+        sgb[wid][pos] = make_double2(bx - ax, by - ay);
+        sgc[wid][pos] = make_double2(cx - ax, cy - ay);
+        sgs[wid][pos] = det * ldexp(1.0, -2 * d) * kInv4Pi;
+        sslot[wid][pos] = ((1 << (2 * d)) - 1) / 3 + (int)path;
       }
       __syncwarp();
-      // (a) cached leaves: r^2 and log only
-      {
-        const int total = nc * Ln;
+      const int total = nm * Ln;
+      if constexpr (MODE == 0) {
         int li = lane / Ln, ni = lane - li * Ln;
         for (int j = lane; j < total; j += 32) {
           const double2 a = sga[wid][li], ba = sgb[wid][li], ca = sgc[wid][li], nn = snxy[ni];
@@ -578,37 +604,50 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, VP_NEAR_MINB)
           ni += 32;
           while (ni >= Ln) { ni -= Ln; ++li; }
         }
-      }
-      // (b) deeper leaves: density by the Koornwinder recurrence
-      const int total = nb * Ln;
-      // nodes j and j + 32 = (li, ni), (lj, nj); lanes strided by 64
-      int li = (nc * Ln + lane) / Ln, ni = nc * Ln + lane - li * Ln;
-      int lj = (nc * Ln + lane + 32) / Ln, nj = nc * Ln + lane + 32 - lj * Ln;
-      for (int j = nc * Ln + lane; j < total; j += 64) {
-        const bool ok2 = j + 32 < total;
-        const int l2 = ok2 ? lj : li, n2 = ok2 ? nj : ni;
-        const double2 ga[2] = {sga[wid][li], sga[wid][l2]}, gb[2] = {sgb[wid][li], sgb[wid][l2]},
-                      gc[2] = {sgc[wid][li], sgc[wid][l2]}, nn[2] = {snxy[ni], snxy[n2]};
-        const double gs[2] = {sgs[wid][li], sgs[wid][l2]}, nwv[2] = {snw[ni], snw[n2]};
-        const bool valid[2] = {true, ok2};
-        acc += near_nodes<P, 2>(ShCoef(cc), sltab, ga, gb, gc, gs, nn, nwv, valid, X0, Y0, E1x, E1y, E2x, E2y,
-                                tx, ty);
-        ni += 64;
-        while (ni >= Ln) { ni -= Ln; ++li; }
-        nj += 64;
-        while (nj >= Ln) { nj -= Ln; ++lj; }
+      } else {
+        // nodes j and j + 32 = (li, ni), (lj, nj); lanes strided by 64
+        int li = lane / Ln, ni = lane - li * Ln;
+        int lj = (lane + 32) / Ln, nj = lane + 32 - lj * Ln;
+        for (int j = lane; j < total; j += 64) {
+          const bool ok2 = j + 32 < total;
+          const int l2 = ok2 ? lj : li, n2 = ok2 ? nj : ni;
+          const double2 ga[2] = {sga[wid][li], sga[wid][l2]}, gb[2] = {sgb[wid][li], sgb[wid][l2]},
+                        gc[2] = {sgc[wid][li], sgc[wid][l2]}, nn[2] = {snxy[ni], snxy[n2]};
+          const double gs[2] = {sgs[wid][li], sgs[wid][l2]}, nwv[2] = {snw[ni], snw[n2]};
+          const bool valid[2] = {true, ok2};
+          acc += near_nodes<P, 2>(ShCoef(scc[MODE == 1 ? wid : 0]), sltab, ga, gb, gc, gs, nn, nwv, valid, X0, Y0,
+                                  E1x, E1y, E2x, E2y, tx, ty);
+          ni += 64;
+          while (ni >= Ln) { ni -= Ln; ++li; }
+          nj += 64;
+          while (nj >= Ln) { nj -= Ln; ++lj; }
+        }
       }
     }
     const double val = warp_sum(acc);
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
-    if (lane == 0) {
-      if (sub_out) {
-        corr[p] = val;
-        sub_out[p] = sub;
-      } else {
-        corr[p] = val - sub;
+    if constexpr (MODE == 0) {
+      const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, exact_zero);
+      if (lane == 0) {
+        part[p] = val;
+        part_s[p] = sub;
       }
+    } else {
+      if (lane == 0) part[p] = val;
     }
+  }
+}
+
+// corr = a + b - s (evaluation) or val = a + b, sub = s (per-pair API)
+__global__ void k_near_combine(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                               const double* __restrict__ s, double* __restrict__ corr, double* __restrict__ sub_out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double v = a[p] + b[p];
+  if (sub_out) {
+    corr[p] = v;
+    sub_out[p] = s[p];
+  } else {
+    corr[p] = v - s[p];
   }
 }
 
@@ -1080,7 +1119,7 @@ struct vp_ctx {
   double ball_factor = 1.5;
   int cache_max_depth = 3, cache_depth = -1;
   int64_t cache_max_bytes = 12ll << 30;
-  DevBuf d_cacheV, d_gcache;
+  DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps;
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
@@ -1278,11 +1317,17 @@ template <int P>
 void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
                      double* corr, double* sub) {
   const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 32);
-  k_near_int<P><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
+  const double* gc = c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr;
+  k_near_int<P, 0><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
       c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-      c->d_rules.as<RulesDev>(), c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr, c->cache_depth, corr,
-      sub);
+      c->d_rules.as<RulesDev>(), gc, c->cache_depth, c->d_npa.as<double>(), c->d_nps.as<double>(), sub != nullptr);
+  k_near_int<P, 1><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
+      c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
+      c->d_rules.as<RulesDev>(), gc, c->cache_depth, c->d_npb.as<double>(), nullptr, sub != nullptr);
+  k_near_combine<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_npa.as<double>(), c->d_npb.as<double>(),
+                                                     c->d_nps.as<double>(), corr, sub);
 }
 
 int build_near_cache(vp_ctx* c);
@@ -1309,10 +1354,13 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
       c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
   if (int rc = build_near_cache(c)) return rc;
+  CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
+  CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
+  CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
   VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub);
   CUDA_TRY(c, cudaGetLastError());
   c->n_leaves_last = nleaves;
-  c->last_launches += 5;
+  c->last_launches += 7;
   if (leaves_host)
     CUDA_TRY(c, cudaMemcpyAsync(leaves_host, c->d_lcnt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
   return 0;
