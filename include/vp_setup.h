@@ -42,6 +42,12 @@ int vps_simplex_rule(int order, int* len, double* x, double* y, double* w);
  * r P_n(2r-1) and r log r P_n(2r-1), n <= ng (ggq.hpp:13-22, :96-182). */
 int vps_ggq(int ng, double* r, double* w, double* max_residual);
 
+/* Circular arc gamma(tau L), tau in [0,1], as a Legendre series of degree
+ * deg (coefficients of P_n(2 tau - 1)); *len = arc length.  Curved-element
+ * input of vp_set_curves. */
+int vps_circle_arc(double cx, double cy, double R, double th0, double th1, int deg, double* gx, double* gy,
+                   double* len);
+
 /* Target nodes on the reference simplex: shifted principal lattice
  * ((i+1)/(p+3), (j+1)/(p+3)), i+j <= p; (p+1)(p+2)/2 nodes. */
 int vps_lattice_nodes(int p, double* x, double* y);

@@ -36,6 +36,8 @@ class VpoProblem(ctypes.Structure):
         ("n_g", ctypes.c_int), ("ggq_r", _d_p), ("ggq_w", _d_p),
         ("eps", ctypes.c_double),
         ("near_model", ctypes.c_int), ("pad_", ctypes.c_int), ("ball_factor", ctypes.c_double),
+        ("curve_id", _i32_p), ("curve_deg", ctypes.c_int), ("pad2_", ctypes.c_int),
+        ("curve_cx", _d_p), ("curve_cy", _d_p), ("curve_len", _d_p),
     ]
 
 
@@ -114,7 +116,7 @@ def _check(rc):
 class Oracle:
     """Holds the arrays of one problem and exposes the oracle entry points."""
 
-    def __init__(self, vxy, tri, p, coeffs, rules, near_model=0, ball_factor=1.5):
+    def __init__(self, vxy, tri, p, coeffs, rules, near_model=0, ball_factor=1.5, curves=None):
         self.vxy = np.ascontiguousarray(vxy, dtype=np.float64).reshape(-1, 2)
         self.tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
         self.coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
@@ -131,6 +133,16 @@ class Oracle:
             n_l=len(k[6]), gl_x=_d(k[6]), gl_w=_d(k[7]),
             n_g=rules.n_g, ggq_r=_d(k[8]), ggq_w=_d(k[9]), eps=rules.eps,
             near_model=near_model, ball_factor=ball_factor)
+        if curves is not None:
+            self._cid = np.ascontiguousarray(curves.curve_id, dtype=np.int32)
+            self._ccx = np.ascontiguousarray(curves.cx, dtype=np.float64)
+            self._ccy = np.ascontiguousarray(curves.cy, dtype=np.float64)
+            self._cl = np.ascontiguousarray(curves.length, dtype=np.float64)
+            self.pr.curve_id = self._cid.ctypes.data_as(_i32_p)
+            self.pr.curve_deg = curves.deg
+            self.pr.curve_cx = _d(self._ccx)
+            self.pr.curve_cy = _d(self._ccy)
+            self.pr.curve_len = _d(self._cl)
 
     @classmethod
     def from_problem(cls, pr, near_model=0, ball_factor=1.5):

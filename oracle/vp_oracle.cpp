@@ -250,6 +250,178 @@ struct QTree {
 };
 
 // ---------------------------------------------------------------------------
+// Curved elements (PAPER.md:1023-1044 blending map,
+// SPEC.md:339-376).  The curved side is gamma(tau L) = G(tau) = sum_n c_n
+// P_n(2 tau - 1); vertices (v0, v1, v2) = (gamma(L), gamma(0), O) so that
+// rho(0,0) = gamma(L), rho(1,0) = gamma(0), rho(0,1) = O.
+// Every operation below has a fixed order that the GPU reproduces with
+// explicitly rounded intrinsics (predicates that decide lists and counts).
+struct CurveC {
+  const double* cx;
+  const double* cy;
+  int D;
+  double L;
+};
+
+void curve_eval(const CurveC& C, double tau, double& gx, double& gy) {
+  const double x = 2.0 * tau - 1.0;
+  double p0 = 1.0, p1 = x;
+  gx = C.cx[0];
+  gy = C.cy[0];
+  if (C.D >= 1) {
+    gx = gx + C.cx[1] * x;
+    gy = gy + C.cy[1] * x;
+  }
+  for (int n = 1; n < C.D; ++n) {
+    const double a = (double)(2 * n + 1) * x;
+    const double b = a * p1;
+    const double c = (double)n * p0;
+    const double p2 = (b - c) / (double)(n + 1);
+    gx = gx + C.cx[n + 1] * p2;
+    gy = gy + C.cy[n + 1] * p2;
+    p0 = p1;
+    p1 = p2;
+  }
+}
+
+// G, dG/dtau and d2G/dtau2 (P'_{n+1} = P'_{n-1} + (2n+1) P_n, same for P'')
+void curve_eval_d(const CurveC& C, double tau, double g[2], double g1[2], double g2[2]) {
+  const double x = 2.0 * tau - 1.0;
+  double p0 = 1.0, p1 = x, d0 = 0.0, d1 = 1.0, e0 = 0.0, e1 = 0.0;
+  g[0] = C.cx[0]; g[1] = C.cy[0];
+  g1[0] = 0.0; g1[1] = 0.0;
+  g2[0] = 0.0; g2[1] = 0.0;
+  if (C.D >= 1) {
+    g[0] = g[0] + C.cx[1] * x; g[1] = g[1] + C.cy[1] * x;
+    g1[0] = g1[0] + C.cx[1] * d1; g1[1] = g1[1] + C.cy[1] * d1;
+  }
+  for (int n = 1; n < C.D; ++n) {
+    const double a = (double)(2 * n + 1) * x;
+    const double p2 = (a * p1 - (double)n * p0) / (double)(n + 1);
+    const double d2 = d0 + (double)(2 * n + 1) * p1;
+    const double e2 = e0 + (double)(2 * n + 1) * d1;
+    g[0] = g[0] + C.cx[n + 1] * p2; g[1] = g[1] + C.cy[n + 1] * p2;
+    g1[0] = g1[0] + C.cx[n + 1] * d2; g1[1] = g1[1] + C.cy[n + 1] * d2;
+    g2[0] = g2[0] + C.cx[n + 1] * e2; g2[1] = g2[1] + C.cy[n + 1] * e2;
+    p0 = p1; p1 = p2; d0 = d1; d1 = d2; e0 = e1; e1 = e2;
+  }
+  g1[0] = 2.0 * g1[0]; g1[1] = 2.0 * g1[1];
+  g2[0] = 4.0 * g2[0]; g2[1] = 4.0 * g2[1];
+}
+
+struct BlendGeom {
+  double PLx, PLy, P0x, P0y, Ox, Oy;
+};
+
+// rho(xi, eta) of PAPER.md eq. for:blend
+void blend(const BlendGeom& B, const CurveC& C, double xi, double eta, double& x, double& y) {
+  const double om = 1.0 - xi;
+  const double lam = om - eta;
+  const double bx = (lam * B.PLx + xi * B.P0x) + eta * B.Ox;
+  const double by = (lam * B.PLy + xi * B.P0y) + eta * B.Oy;
+  if (!(om > 1e-13)) {  // xi -> 1 limit: the bracket vanishes
+    x = bx;
+    y = by;
+    return;
+  }
+  double gx, gy;
+  curve_eval(C, om, gx, gy);
+  const double Dx = (gx - om * B.PLx) - xi * B.P0x;
+  const double Dy = (gy - om * B.PLy) - xi * B.P0y;
+  const double r = lam / om;
+  x = bx + r * Dx;
+  y = by + r * Dy;
+}
+
+// rho and its Jacobian [dx/dxi dx/deta; dy/dxi dy/deta]
+void blend_jac(const BlendGeom& B, const CurveC& C, double xi, double eta, double& x, double& y,
+               double J[4]) {
+  const double om0 = 1.0 - xi;
+  const double om = om0 > 1e-13 ? om0 : 1e-13;
+  const double lam = om0 - eta;
+  double g[2], g1[2], g2[2];
+  curve_eval_d(C, om, g, g1, g2);
+  const double bx = (lam * B.PLx + xi * B.P0x) + eta * B.Ox;
+  const double by = (lam * B.PLy + xi * B.P0y) + eta * B.Oy;
+  const double Dx = (g[0] - om * B.PLx) - xi * B.P0x;
+  const double Dy = (g[1] - om * B.PLy) - xi * B.P0y;
+  const double r = lam / om;
+  x = bx + r * Dx;
+  y = by + r * Dy;
+  const double drx = -eta / (om * om), dre = -1.0 / om;
+  const double dDx = (B.PLx - g1[0]) - B.P0x, dDy = (B.PLy - g1[1]) - B.P0y;
+  J[0] = ((B.P0x - B.PLx) + drx * Dx) + r * dDx;
+  J[1] = (B.Ox - B.PLx) + dre * Dx;
+  J[2] = ((B.P0y - B.PLy) + drx * Dy) + r * dDy;
+  J[3] = (B.Oy - B.PLy) + dre * Dy;
+}
+
+constexpr int kBlendNewton = 12;  // fixed count: identical iterates on CPU and GPU
+
+// Newton inverse of the blending map seeded by (xi, eta)
+void blend_inverse(const BlendGeom& B, const CurveC& C, double tx, double ty, double& xi, double& eta) {
+  for (int it = 0; it < kBlendNewton; ++it) {
+    double x, y, J[4];
+    blend_jac(B, C, xi, eta, x, y, J);
+    const double rx = tx - x, ry = ty - y;
+    const double dj = J[0] * J[3] - J[1] * J[2];
+    const double dxi = (J[3] * rx - J[1] * ry) / dj;
+    const double deta = (J[0] * ry - J[2] * rx) / dj;
+    xi = xi + dxi;
+    eta = eta + deta;
+  }
+}
+
+// Newton inverse to convergence (quadrature points; values, not predicates)
+void blend_inverse_tol(const BlendGeom& B, const CurveC& C, double tx, double ty, double& xi, double& eta) {
+  for (int it = 0; it < 40; ++it) {
+    double x, y, J[4];
+    blend_jac(B, C, xi, eta, x, y, J);
+    const double rx = tx - x, ry = ty - y;
+    const double dj = J[0] * J[3] - J[1] * J[2];
+    const double dxi = (J[3] * rx - J[1] * ry) / dj;
+    const double deta = (J[0] * ry - J[2] * rx) / dj;
+    xi = xi + dxi;
+    eta = eta + deta;
+    if (std::abs(dxi) + std::abs(deta) < 1e-15) break;
+  }
+}
+
+// s~ = argmin_s |v - gamma(s)| on the curved side gamma(s) = G(1 - s/L):
+// best of 33 samples, then 10 Newton steps on (gamma - v).gamma' = 0,
+// clamped to [0, L] (SPEC.md:537 asks golden section + Newton; any exact
+// minimiser gives the same panels).
+double curved_argmin(const CurveC& C, double vx, double vy) {
+  const double L = C.L;
+  int best = 0;
+  double bd = 1e300;
+  for (int i = 0; i <= 32; ++i) {
+    double gx, gy;
+    curve_eval(C, 1.0 - (double)i / 32.0, gx, gy);
+    const double dx = gx - vx, dy = gy - vy;
+    const double d2 = dx * dx + dy * dy;
+    if (d2 < bd) {
+      bd = d2;
+      best = i;
+    }
+  }
+  double s = L * ((double)best / 32.0);
+  for (int it = 0; it < 10; ++it) {
+    double g[2], g1[2], g2[2];
+    curve_eval_d(C, 1.0 - s / L, g, g1, g2);
+    const double tx = -g1[0] / L, ty = -g1[1] / L;       // gamma'(s)
+    const double ax = g2[0] / (L * L), ay = g2[1] / (L * L);  // gamma''(s)
+    const double dx = g[0] - vx, dy = g[1] - vy;
+    const double phi = dx * tx + dy * ty;
+    const double dphi = (tx * tx + ty * ty) + (dx * ax + dy * ay);
+    if (!(dphi > 0.0)) break;
+    s = s - phi / dphi;
+    s = std::min(std::max(s, 0.0), L);
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
 // Per-problem setup: element geometry, near-field models, sources.
 struct Setup {
   const vpo_problem* pr = nullptr;
@@ -267,6 +439,32 @@ struct Setup {
   std::vector<double> corners;
   // sources
   std::vector<double> sx, sy, sq;
+
+  bool curved(int64_t e) const { return pr->curve_id && pr->curve_id[e] >= 0; }
+  CurveC curve(int64_t e) const {
+    const int c = pr->curve_id[e], D = pr->curve_deg;
+    return CurveC{pr->curve_cx + (int64_t)c * (D + 1), pr->curve_cy + (int64_t)c * (D + 1), D, pr->curve_len[c]};
+  }
+  BlendGeom bgeom(int64_t e) const {
+    const int32_t* id = pr->tri + 3 * e;
+    return BlendGeom{pr->vxy[2 * id[0]], pr->vxy[2 * id[0] + 1], pr->vxy[2 * id[1]], pr->vxy[2 * id[1] + 1],
+                     pr->vxy[2 * id[2]], pr->vxy[2 * id[2] + 1]};
+  }
+  // element map (affine or blending) at a reference point, and |J| there
+  void map_point(int64_t e, double xi, double eta, double& x, double& y) const {
+    if (curved(e)) {
+      blend(bgeom(e), curve(e), xi, eta, x, y);
+      return;
+    }
+    x = x0[e] + (xi * e1x[e] + eta * e2x[e]);
+    y = y0[e] + (xi * e1y[e] + eta * e2y[e]);
+  }
+  double jac_at(int64_t e, double xi, double eta) const {
+    if (!curved(e)) return det[e];
+    double x, y, J[4];
+    blend_jac(bgeom(e), curve(e), xi, eta, x, y, J);
+    return std::abs(J[0] * J[3] - J[1] * J[2]);
+  }
 
   int init(const vpo_problem* p, bool want_lists, bool want_sources) {
     pr = p;
@@ -345,6 +543,16 @@ struct Setup {
           lox = std::min(lox, mx - r); hix = std::max(hix, mx + r);
           loy = std::min(loy, my - r); hiy = std::max(hiy, my + r);
         }
+        if (curved(e)) {  // the element itself (for locate) bulges past its chord
+          const CurveC C = curve(e);
+          for (int k = 0; k <= 32; ++k) {
+            double gx, gy;
+            curve_eval(C, k / 32.0, gx, gy);
+            const double pad = 1e-9 * C.L + 1e-300;
+            lox = std::min(lox, gx - 0.05 * C.L - pad); hix = std::max(hix, gx + 0.05 * C.L + pad);
+            loy = std::min(loy, gy - 0.05 * C.L - pad); hiy = std::max(hiy, gy + 0.05 * C.L + pad);
+          }
+        }
         bb[4 * e] = lox; bb[4 * e + 1] = loy; bb[4 * e + 2] = hix; bb[4 * e + 3] = hiy;
       }
       // quadtree over the four corners of every near-field bbox
@@ -368,11 +576,10 @@ struct Setup {
         const double* c = p->coeffs + e * M;
         for (int i = 0; i < L; ++i) {
           const double xi = p->far_x[i], eta = p->far_y[i];
-          sx[e * L + i] = x0[e] + (xi * e1x[e] + eta * e2x[e]);
-          sy[e * L + i] = y0[e] + (xi * e1y[e] + eta * e2y[e]);
+          map_point(e, xi, eta, sx[e * L + i], sy[e * L + i]);
           const double f = density(p->p, c, xi, eta);
           // q_i = w_i |J_T| f(y_i) / (4 pi): sum q log r^2 = (1/2pi) sum w|J|f log r
-          sq[e * L + i] = (p->far_w[i] * det[e]) * f * kInv4Pi;
+          sq[e * L + i] = (p->far_w[i] * jac_at(e, xi, eta)) * f * kInv4Pi;
         }
       }
     }
@@ -389,6 +596,18 @@ struct Setup {
     xi = a0 + a1;
     const double b0 = i10 * dx, b1 = i11 * dy;
     eta = b0 + b1;
+    if (curved(e)) {
+      // blending-map inverse seeded by the chord's affine inverse, with a
+      // residual check so a non-converged iterate never counts as inside
+      const BlendGeom B = bgeom(e);
+      const CurveC C = curve(e);
+      blend_inverse(B, C, tx, ty, xi, eta);
+      double x, y;
+      blend(B, C, xi, eta, x, y);
+      const double rx = tx - x, ry = ty - y;
+      const double tolr = 1e-9 * C.L;
+      if (!(rx * rx + ry * ry <= tolr * tolr)) return false;
+    }
     const double l0 = (1.0 - xi) - eta;
     return xi >= -kBaryTol && eta >= -kBaryTol && l0 >= -kBaryTol;
   }
@@ -495,8 +714,13 @@ struct Setup {
     const double X0 = x0[e], Y0 = y0[e];
     const double E1x = e1x[e], E1y = e1y[e], E2x = e2x[e], E2y = e2y[e];
     const double* vv[3] = {a, b, c};
+    const bool cv = curved(e);
     double px[3], py[3];
     for (int k = 0; k < 3; ++k) {
+      if (cv) {
+        blend(bgeom(e), curve(e), vv[k][0], vv[k][1], px[k], py[k]);
+        continue;
+      }
       const double s0 = vv[k][0] * E1x, s1 = vv[k][1] * E2x;
       px[k] = X0 + (s0 + s1);
       const double t0 = vv[k][0] * E1y, t1 = vv[k][1] * E2y;
@@ -526,7 +750,14 @@ struct Setup {
       bool nearp = false;
       for (int k = 0; k < 3 && !nearp; ++k) {
         const int k1 = (k + 1) % 3;
-        const double ta = g * (l0[k] * sc);
+        double len;
+        if (cv) {  // curved map: sub-simplices are not congruent; use their mapped chords
+          const double sxk = px[k1] - px[k], syk = py[k1] - py[k];
+          len = std::sqrt(sxk * sxk + syk * syk);
+        } else {
+          len = l0[k] * sc;
+        }
+        const double ta = g * len;
         if (dist[k] + dist[k1] < ta) nearp = true;
       }
       accept = !nearp;
@@ -541,13 +772,14 @@ struct Setup {
         const double u = pr->near_x[i], v = pr->near_y[i];
         const double xi = a[0] + (u * (b[0] - a[0]) + v * (c[0] - a[0]));
         const double eta = a[1] + (u * (b[1] - a[1]) + v * (c[1] - a[1]));
-        const double yx = X0 + (xi * E1x + eta * E2x);
-        const double yy = Y0 + (xi * E1y + eta * E2y);
+        double yx, yy;
+        map_point(e, xi, eta, yx, yy);
         const double f = density(pr->p, cf, xi, eta);
         const double dx = tx - yx, dy = ty - yy;
-        s += pr->near_w[i] * f * std::log(dx * dx + dy * dy);
+        const double jw = cv ? jac_at(e, xi, eta) : 1.0;
+        s += pr->near_w[i] * jw * f * std::log(dx * dx + dy * dy);
       }
-      acc.sum += s * (det[e] * std::ldexp(1.0, -2 * d)) * kInv4Pi;
+      acc.sum += s * ((cv ? 1.0 : det[e]) * std::ldexp(1.0, -2 * d)) * kInv4Pi;
       return;
     }
     const double mab[2] = {(a[0] + b[0]) * 0.5, (a[1] + b[1]) * 0.5};
@@ -573,7 +805,115 @@ struct Setup {
     double sum = 0.0;
     int64_t panels = 0, degenerate = 0;
   };
+  // panel boundaries of [0, L] refined toward st
+  static void panels_of(double st, double L, double dmin, std::vector<double>& bnd) {
+    int N = 0;
+    for (double x = st; !(x < dmin); x *= 0.5) ++N;
+    int Mm = 0;
+    for (double x = L - st; !(x < dmin); x *= 0.5) ++Mm;
+    bnd.clear();
+    bnd.push_back(0.0);
+    for (int i = 1; i <= N; ++i) bnd.push_back(st - std::ldexp(st, -i));
+    bnd.push_back(st);
+    for (int i = Mm; i >= 1; --i) bnd.push_back(st + std::ldexp(L - st, -i));
+    bnd.push_back(L);
+  }
+
+  // self_eval on a curved element: sub-element (t, gamma)
+  // with Jacobian |(gamma(s) - t) x gamma'(s)| and r0(s) = |gamma(s) - t|;
+  // the two straight sub-triangles as for triangles; the density at every
+  // quadrature point through the Newton inverse of the blending map seeded
+  // on the (r, s) line in reference coordinates.
+  void self_eval_curved(int64_t e, double tx, double ty, double txi, double teta, SelfAcc& acc) const {
+    const BlendGeom B = bgeom(e);
+    const CurveC C = curve(e);
+    const double* cf = pr->coeffs + e * M;
+    const double vx[3] = {B.PLx, B.P0x, B.Ox}, vy[3] = {B.PLy, B.P0y, B.Oy};
+    const double refx[3] = {0.0, 1.0, 0.0}, refy[3] = {0.0, 0.0, 1.0};
+    double total = 0.0;
+    std::vector<double> bnd;
+    for (int k = 0; k < 3; ++k) {
+      const int k1 = (k + 1) % 3;
+      double L, st, dmin, hconst = 0.0;
+      const bool arc = (k == 0);
+      if (arc) {
+        L = C.L;
+        st = curved_argmin(C, tx, ty);
+        double gx, gy;
+        curve_eval(C, 1.0 - st / L, gx, gy);
+        dmin = std::sqrt((tx - gx) * (tx - gx) + (ty - gy) * (ty - gy));
+        if (!(dmin > 1e-13 * L)) {
+          acc.degenerate++;
+          continue;
+        }
+      } else {
+        const double ABx = vx[k1] - vx[k], ABy = vy[k1] - vy[k];
+        L = std::sqrt(ABx * ABx + ABy * ABy);
+        const double vAx = tx - vx[k], vAy = ty - vy[k];
+        const double cr = ABx * vAy - ABy * vAx;
+        hconst = std::abs(cr) / L;
+        if (!(hconst > 1e-13 * L)) {
+          acc.degenerate++;
+          continue;
+        }
+        const double sp = (vAx * ABx + vAy * ABy) / L;
+        st = std::min(std::max(sp, 0.0), L);
+        const double gx = vx[k] + (st / L) * ABx, gy = vy[k] + (st / L) * ABy;
+        dmin = std::sqrt((tx - gx) * (tx - gx) + (ty - gy) * (ty - gy));
+      }
+      panels_of(st, L, dmin, bnd);
+      double sub = 0.0;
+      for (size_t pi = 0; pi + 1 < bnd.size(); ++pi) {
+        const double s0 = bnd[pi], s1 = bnd[pi + 1];
+        if (!(s1 > s0)) continue;
+        acc.panels++;
+        const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
+        for (int gq = 0; gq < pr->n_l; ++gq) {
+          const double s = mid + half * pr->gl_x[gq];
+          const double ws = half * pr->gl_w[gq];
+          const double sl = s / L;
+          double px, py, jf, grx, gry;
+          if (arc) {
+            double g[2], g1[2], g2[2];
+            curve_eval_d(C, 1.0 - sl, g, g1, g2);
+            px = g[0];
+            py = g[1];
+            const double tgx = -g1[0] / L, tgy = -g1[1] / L;
+            jf = std::abs((px - tx) * tgy - (py - ty) * tgx);
+            grx = sl;  // rho(xi, 0) = G(1 - xi) = gamma(xi L)
+            gry = 0.0;
+          } else {
+            px = vx[k] + sl * (vx[k1] - vx[k]);
+            py = vy[k] + sl * (vy[k1] - vy[k]);
+            jf = hconst;
+            grx = refx[k] + sl * (refx[k1] - refx[k]);
+            gry = refy[k] + sl * (refy[k1] - refy[k]);
+          }
+          const double r0 = std::sqrt((px - tx) * (px - tx) + (py - ty) * (py - ty));
+          const double lr0 = std::log(r0);
+          double inner = 0.0;
+          for (int j = 0; j <= pr->n_g; ++j) {
+            const double rj = pr->ggq_r[j];
+            const double yx = tx + rj * (px - tx), yy = ty + rj * (py - ty);
+            double xi = txi + rj * (grx - txi), eta = teta + rj * (gry - teta);
+            blend_inverse_tol(B, C, yx, yy, xi, eta);
+            const double f = density(pr->p, cf, std::min(std::max(xi, 0.0), 1.0),
+                                     std::min(std::max(eta, 0.0), 1.0 - std::min(std::max(xi, 0.0), 1.0)));
+            inner += pr->ggq_w[j] * rj * (lr0 + std::log(rj)) * f;
+          }
+          sub += ws * jf * inner;
+        }
+      }
+      total += sub;
+    }
+    acc.sum += total * kInv2Pi;
+  }
+
   void self_eval(int64_t e, double tx, double ty, double txi, double teta, SelfAcc& acc) const {
+    if (curved(e)) {
+      self_eval_curved(e, tx, ty, txi, teta, acc);
+      return;
+    }
     const int32_t* id = pr->tri + 3 * e;
     const double refx[3] = {0.0, 1.0, 0.0}, refy[3] = {0.0, 0.0, 1.0};
     const double* cf = pr->coeffs + e * M;
@@ -850,11 +1190,9 @@ int vpo_self(const vpo_problem* pr, double tx, double ty, int32_t elem, double* 
   Setup s;
   if (int rc = s.init(pr, false, true)) return rc;
   if (elem < 0 || elem >= s.E) return fail(1, "self: element out of range");
-  // reference coordinates via the inverse affine map
-  const double i00 = s.e2y[elem] / s.det[elem], i01 = -s.e2x[elem] / s.det[elem];
-  const double i10 = -s.e1y[elem] / s.det[elem], i11 = s.e1x[elem] / s.det[elem];
-  const double dx = tx - s.x0[elem], dy = ty - s.y0[elem];
-  const double xi = i00 * dx + i01 * dy, eta = i10 * dx + i11 * dy;
+  // reference coordinates via the inverse element map
+  double xi, eta;
+  s.ref_coords(elem, tx, ty, xi, eta);
   Setup::SelfAcc acc;
   s.self_eval(elem, tx, ty, xi, eta, acc);
   if (val) *val = acc.sum;

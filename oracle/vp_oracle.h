@@ -49,6 +49,15 @@ typedef struct {
   int near_model;      /* 0 precise (Bernstein ellipses), 1 ball */
   int pad_;
   double ball_factor;  /* ball = circumscribed circle scaled by this (1.5) */
+  /* curved (blending-map) elements: curve_id[e] >= 0 marks
+   * element e as curved with vertex order (gamma(L), gamma(0), O) and its
+   * side gamma(tau L) = sum_n c_n P_n(2 tau - 1), tau in [0,1]; NULL = all straight */
+  const int32_t* curve_id;
+  int curve_deg;
+  int pad2_;
+  const double* curve_cx; /* [n_curves * (curve_deg+1)] */
+  const double* curve_cy;
+  const double* curve_len;
 } vpo_problem;
 
 typedef struct {

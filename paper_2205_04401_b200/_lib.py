@@ -97,6 +97,8 @@ _SIGS = [
     ("vps_simplex_rule", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_double_p,
                                         c_double_p, c_double_p]),
     ("vps_ggq", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p, c_double_p]),
+    ("vps_circle_arc", ctypes.c_int, [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_int, c_double_p, c_double_p, c_double_p]),
     ("vps_lattice_nodes", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p]),
     ("vps_density_eval", ctypes.c_double, [ctypes.c_int, c_double_p, ctypes.c_int, ctypes.c_double,
                                            ctypes.c_double]),

@@ -237,6 +237,52 @@ def load_config(cfg: int, q_override: int = 0, seed: int = 0, with_rules: bool =
     return pr
 
 
+@dataclass
+class Curves:
+    """Curved (blending-map) elements: curve_id[e] >= 0 marks element e as
+    curved, vertex order (gamma(L), gamma(0), O); its side is
+    gamma(tau L) = sum_n (cx, cy)[curve_id, n] P_n(2 tau - 1)."""
+    curve_id: np.ndarray
+    deg: int
+    cx: np.ndarray
+    cy: np.ndarray
+    length: np.ndarray
+
+
+def circle_arc(cx, cy, R, th0, th1, deg=16):
+    gx, gy, ln = np.zeros(deg + 1), np.zeros(deg + 1), ctypes.c_double()
+    _check(_lib.lib().vps_circle_arc(cx, cy, R, th0, th1, deg, _d(gx), _d(gy), ctypes.byref(ln)), _setup_err())
+    return gx, gy, ln.value
+
+
+def curve_boundary_of_disk(vxy, tri, R=1.0, deg=16, tol=1e-12):
+    """Turn every triangle of a disk mesh with an edge on |x| = R into a
+    curved element on the exact circle (vertices reordered to
+    (gamma(L), gamma(0), O), counter-clockwise).  Returns (tri, Curves)."""
+    vxy = np.asarray(vxy, dtype=np.float64)
+    tri = np.array(tri, dtype=np.int32).reshape(-1, 3).copy()
+    on = np.abs(np.hypot(vxy[:, 0], vxy[:, 1]) - R) <= tol
+    cid = -np.ones(len(tri), dtype=np.int32)
+    cxs, cys, lens = [], [], []
+    for e, t in enumerate(tri):
+        flags = on[t]
+        if flags.sum() != 2:
+            continue
+        k = int(np.nonzero(~flags)[0][0])  # the interior vertex O
+        a, b, o = t[(k + 1) % 3], t[(k + 2) % 3], t[k]  # CCW (A, B, O)
+        tri[e] = (a, b, o)
+        tha = np.arctan2(vxy[a, 1], vxy[a, 0])
+        thb = np.arctan2(vxy[b, 1], vxy[b, 0])
+        if thb < tha:
+            thb += 2 * np.pi
+        gx, gy, ln = circle_arc(0.0, 0.0, R, thb, tha, deg)  # gamma(0) = B -> gamma(L) = A
+        cid[e] = len(lens)
+        cxs.append(gx)
+        cys.append(gy)
+        lens.append(ln)
+    return tri, Curves(cid, deg, np.array(cxs), np.array(cys), np.array(lens))
+
+
 # ---------------------------------------------------------------------------
 # evaluator (GPU, through the C-ABI)
 

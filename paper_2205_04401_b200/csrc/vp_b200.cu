@@ -212,9 +212,16 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 #ifndef VP_FAR_MINB
 #define VP_FAR_MINB 2
 #endif
-constexpr int FAR_THREADS = 256;
+#ifndef VP_FAR_UNROLL
+#define VP_FAR_UNROLL 2
+#endif
+#ifndef VP_FAR_THREADS
+#define VP_FAR_THREADS 256
+#endif
+constexpr int FAR_THREADS = VP_FAR_THREADS;
 constexpr int FAR_R = VP_FAR_R;      // targets per thread (register tile)
 constexpr int FAR_TILE = 256;        // sources per shared-memory tile
+constexpr int kFarUnroll = VP_FAR_UNROLL;
 
 __device__ double2 g_logtab[kLogEntries];  // {r_k, -log r_k}, filled at vp_create
 
@@ -244,12 +251,12 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
   for (int64_t base = s0; base < s1; base += FAR_TILE) {
     const int n = (int)min((int64_t)FAR_TILE, s1 - base);
     __syncthreads();
-    if (threadIdx.x < n) {
-      sxy[threadIdx.x] = make_double2(sx[base + threadIdx.x], sy[base + threadIdx.x]);
-      ssq[threadIdx.x] = sq[base + threadIdx.x];
+    for (int j = threadIdx.x; j < n; j += FAR_THREADS) {
+      sxy[j] = make_double2(sx[base + j], sy[base + j]);
+      ssq[j] = sq[base + j];
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll (kFarUnroll)
     for (int j = 0; j < n; ++j) {
       const double2 ps = sxy[j];
       const double q = ssq[j];

@@ -390,6 +390,56 @@ int vps_ggq(int ng, double* rout, double* wout, double* max_residual) {
   return fail(2, "ggq: moment fitting failed to converge");
 }
 
+// Arc-length parametrised circular arc as a Legendre series on tau in [0,1]:
+// G(tau) = (cx, cy) + R (cos th(tau), sin th(tau)), th = th0 + tau (th1 - th0);
+// coefficients by Gauss-Legendre projection (exact to rounding for deg >= 16
+// on arcs of a mesh-sized angle).  *len = R |th1 - th0|.
+int vps_circle_arc(double cx, double cy, double R, double th0, double th1, int deg, double* gx, double* gy,
+                   double* len) {
+  if (deg < 1 || deg > 40 || !gx || !gy || !(R > 0.0)) return fail(1, "circle_arc: deg in [1,40], R > 0");
+  // Gauss-Legendre in long double: a double rule leaves ~1e-14 noise in the
+  // tail coefficients, which the curved-element tests resolve.
+  const int nq = deg + 12;
+  std::vector<long double> x(nq), w(nq);
+  for (int i = 0; i < nq; ++i) {
+    long double z = cosl(3.14159265358979323846264338L * (i + 0.75L) / (nq + 0.5L)), dp = 0.0L;
+    for (int it = 0; it < 100; ++it) {
+      long double p0 = 1.0L, p1 = z;
+      for (int k = 1; k < nq; ++k) {
+        const long double p2 = ((2 * k + 1) * z * p1 - k * p0) / (k + 1);
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = nq * (p0 - z * p1) / (1.0L - z * z);
+      const long double dz = p1 / dp;
+      z -= dz;
+      if (fabsl(dz) < 1e-19L) break;
+    }
+    x[i] = z;
+    w[i] = 2.0L / ((1.0L - z * z) * dp * dp);
+  }
+  for (int n = 0; n <= deg; ++n) {
+    long double ax = 0.0L, ay = 0.0L;
+    for (int i = 0; i < nq; ++i) {
+      const long double tau = 0.5L * (1.0L + x[i]);
+      const long double th = th0 + tau * ((long double)th1 - th0);
+      long double p0 = 1.0L, pn = x[i];
+      if (n == 0) pn = 1.0L;
+      for (int k = 1; k < n; ++k) {
+        const long double p2 = ((2 * k + 1) * x[i] * pn - k * p0) / (k + 1);
+        p0 = pn;
+        pn = p2;
+      }
+      ax += w[i] * (cx + R * cosl(th)) * pn;
+      ay += w[i] * (cy + R * sinl(th)) * pn;
+    }
+    gx[n] = (double)(ax * (2 * n + 1) / 2.0L);
+    gy[n] = (double)(ay * (2 * n + 1) / 2.0L);
+  }
+  if (len) *len = R * std::abs(th1 - th0);
+  return 0;
+}
+
 int vps_lattice_nodes(int p, double* x, double* y) {
   if (p < 0 || p > vp::kMaxP || !x || !y) return fail(1, "lattice: order out of range");
   int k = 0;

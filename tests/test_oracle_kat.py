@@ -220,3 +220,56 @@ def test_ball_model_lists_match_brute_force_and_is_coarser_on_the_disk():
     _, _, stb = Ob.evaluate(sub)
     _, _, stp = Oracle.from_problem(pr).evaluate(sub)
     assert stp["n_near_pairs"] < stb["n_near_pairs"] and stp["n_leaves"] < stb["n_leaves"]
+
+
+# ---------------------------------------------------------------------------
+# curved (blending-map) elements, SURVEY.md §8(f3)
+
+def _disk_sample(stride=617):
+    pr = vp.load_config(2)
+    return pr, pr.txy[::stride]
+
+
+def test_circle_arc_coefficients_reproduce_the_arc():
+    gx, gy, ln = vp.circle_arc(0.5, -0.25, 2.0, 0.3, 0.1, deg=16)
+    assert abs(ln - 0.4) < 1e-15
+    tau = np.linspace(0, 1, 41)
+    from numpy.polynomial import legendre as L
+    x, y = L.legval(2 * tau - 1, gx), L.legval(2 * tau - 1, gy)
+    th = 0.3 + tau * (0.1 - 0.3)
+    assert np.abs(x - (0.5 + 2 * np.cos(th))).max() < 1e-15
+    assert np.abs(y - (-0.25 + 2 * np.sin(th))).max() < 1e-15
+
+
+def test_curved_disk_constant_density_is_exact():
+    """f = 1 on the exact unit disk: u = (|x|^2 - 1)/4.  The polygonal mesh
+    misses it by its O(h^2) domain error; blended boundary elements reach eps."""
+    pr, sub = _disk_sample()
+    tri, cv = vp.curve_boundary_of_disk(pr.vxy, pr.tri)
+    assert (cv.curve_id >= 0).sum() == 256
+    co = const_coeffs(len(tri), pr.p)
+    r = vp.make_rules(50, eps=1e-12)
+    exact = (np.sum(sub ** 2, 1) - 1) / 4
+    u, _, _ = Oracle(pr.vxy, tri, pr.p, co, r, curves=cv).evaluate(sub)
+    us, _, _ = Oracle(pr.vxy, tri, pr.p, co, r).evaluate(sub)
+    assert np.abs(u - exact).max() < 5e-12
+    assert np.abs(us - exact).max() > 1e-10
+
+
+def test_curved_element_with_straight_side_equals_straight_element():
+    """A blending map over a straight gamma is the affine map, so marking an
+    element curved with its chord as gamma must not change u."""
+    pr, sub = _disk_sample(stride=1201)
+    tri, cv = vp.curve_boundary_of_disk(pr.vxy, pr.tri)
+    chord = np.zeros_like(cv.cx), np.zeros_like(cv.cy)
+    for e in np.nonzero(cv.curve_id >= 0)[0]:
+        c = cv.curve_id[e]
+        a, b = pr.vxy[tri[e, 0]], pr.vxy[tri[e, 1]]  # gamma(L) = a, gamma(0) = b
+        chord[0][c, 0], chord[0][c, 1] = (a[0] + b[0]) / 2, (a[0] - b[0]) / 2
+        chord[1][c, 0], chord[1][c, 1] = (a[1] + b[1]) / 2, (a[1] - b[1]) / 2
+    flat = vp.Curves(cv.curve_id, cv.deg, chord[0], chord[1], np.hypot(chord[0][:, 1], chord[1][:, 1]) * 2)
+    r = vp.make_rules(50, eps=1e-12)
+    co = vp.project_density(pr.vxy, tri, pr.p, vp.F_GAUSS, [0.2, -0.1, 3.0])
+    u1, _, _ = Oracle(pr.vxy, tri, pr.p, co, r, curves=flat).evaluate(sub)
+    u0, _, _ = Oracle(pr.vxy, tri, pr.p, co, r).evaluate(sub)
+    assert np.abs(u1 - u0).max() < 1e-12 * max(1.0, np.abs(u0).max())
