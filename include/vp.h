@@ -88,6 +88,18 @@ const char* vp_last_error(const vp_ctx* ctx);
 int vp_set_mesh(vp_ctx* ctx, int64_t n_vert, const double* vxy, int64_t n_tri,
                 const int32_t* tri);
 
+/* Curved (blending-map) elements; replaces the reference's
+ * per-element `kind/curve/s_a/s_b` fields of TriMesh (SPEC.md:171-179,
+ * :339-376) with a Legendre series per curve.  curve_id[e] >= 0 marks
+ * triangle e as curved: its vertices are (gamma(L), gamma(0), O) and its side
+ * from vertex 1 to vertex 0 is gamma(tau L) = sum_n (cx, cy)[id*(deg+1) + n]
+ * P_n(2 tau - 1), tau in [0, 1], of arc length len[id].  The map is the
+ * blending map of PAPER.md eq. for:blend; sources, lists (Newton locate),
+ * near and self quadrature follow it.  curve_id == NULL clears; a new mesh
+ * clears.  Call after vp_set_mesh. */
+int vp_set_curves(vp_ctx* ctx, const int32_t* curve_id, int deg, int64_t n_curves, const double* cx,
+                  const double* cy, const double* len);
+
 /* Rules + tolerance; builds the per-element near-field models
  * (build_model) on the host so list predicates are
  * bit-reproducible, and the element bins used by the list build. */

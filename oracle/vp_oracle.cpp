@@ -842,10 +842,11 @@ struct Setup {
         double gx, gy;
         curve_eval(C, 1.0 - st / L, gx, gy);
         dmin = std::sqrt((tx - gx) * (tx - gx) + (ty - gy) * (ty - gy));
-        if (!(dmin > 1e-13 * L)) {
-          acc.degenerate++;
-          continue;
-        }
+        // t on the arc: unlike a straight side, the sub-element (t, gamma)
+        // keeps its area (the lens between the arc and the chords from t),
+        // so it is not skipped; its integrand vanishes like
+        // (s - s~)^2 log|s - s~| at s~, and the panels refine to 1e-9 L
+        if (!(dmin > 1e-13 * L)) dmin = 1e-9 * L;
       } else {
         const double ABx = vx[k1] - vx[k], ABy = vy[k1] - vy[k];
         L = std::sqrt(ABx * ABx + ABy * ABy);

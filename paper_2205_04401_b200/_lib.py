@@ -66,6 +66,8 @@ _SIGS = [
     ("vp_destroy", None, [ctypes.c_void_p]),
     ("vp_last_error", ctypes.c_char_p, [ctypes.c_void_p]),
     ("vp_set_mesh", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, ctypes.c_int64, c_int32_p]),
+    ("vp_set_curves", ctypes.c_int, [ctypes.c_void_p, c_int32_p, ctypes.c_int, ctypes.c_int64, c_double_p,
+                                     c_double_p, c_double_p]),
     ("vp_set_rules", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(VpRules)]),
     ("vp_set_density", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_double_p]),
     ("vp_build_nearlist", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_int32_p,

@@ -329,6 +329,18 @@ class Evaluator:
                                    _i32(self._tri)), self._err())
         self.n_tri = self._tri.shape[0]
 
+    def set_curves(self, curves: "Curves | None"):
+        """Curved (blending-map) elements; None clears."""
+        if curves is None:
+            _check(self._L.vp_set_curves(self._h, None, 0, 0, None, None, None), self._err())
+            return
+        self._cid = np.ascontiguousarray(curves.curve_id, dtype=np.int32)
+        self._ccx = np.ascontiguousarray(curves.cx, dtype=np.float64)
+        self._ccy = np.ascontiguousarray(curves.cy, dtype=np.float64)
+        self._cl = np.ascontiguousarray(curves.length, dtype=np.float64)
+        _check(self._L.vp_set_curves(self._h, _i32(self._cid), curves.deg, self._cl.size, _d(self._ccx),
+                                     _d(self._ccy), _d(self._cl)), self._err())
+
     def set_rules(self, rules: Rules):
         self._rules_struct = rules.as_struct()
         self._rules = rules

@@ -24,6 +24,7 @@
 #include "vp.h"
 #include "vp_setup.h"
 #include "vp_device.cuh"
+#include "vp_curve.cuh"
 
 using namespace vp;
 
@@ -53,6 +54,54 @@ struct GridDev {
   double x0, y0, cs, inv_cs;
   int nx, ny;
 };
+
+// curved elements (vp_curve.cuh): element -> curve, blending geometry
+__device__ __forceinline__ int curve_id_of(const CurvesDev& CV, int64_t e) { return CV.ecurve ? CV.ecurve[e] : -1; }
+__device__ __forceinline__ CurveRef curve_of(const CurvesDev& CV, int c) {
+  return CurveRef{CV.cx + (int64_t)c * (CV.D + 1), CV.cy + (int64_t)c * (CV.D + 1), CV.D, CV.len[c]};
+}
+__device__ __forceinline__ BlendGeom bgeom_of(const ElemRec& E) {
+  return BlendGeom{E.x0, E.y0, E.x1, E.y1, E.x2, E.y2};
+}
+
+// containment in a curved element (oracle ref_coords, curved branch): the
+// chord's affine inverse seeds 12 Newton steps of the blending-map inverse;
+// a residual above 1e-9 L never counts as inside
+__device__ __forceinline__ bool rn_locate_curved(const ElemRec& E, const CurveRef& C, double tx, double ty,
+                                                 double& xi, double& eta) {
+  const double dx = rn_sub(tx, E.x0), dy = rn_sub(ty, E.y0);
+  xi = rn_add(rn_mul(E.i00, dx), rn_mul(E.i01, dy));
+  eta = rn_add(rn_mul(E.i10, dx), rn_mul(E.i11, dy));
+  const BlendGeom B = bgeom_of(E);
+  blend_inverse<true>(B, C, tx, ty, xi, eta);
+  double x, y;
+  blend<true>(B, C, xi, eta, x, y);
+  const double rx = rn_sub(tx, x), ry = rn_sub(ty, y);
+  const double tolr = rn_mul(1e-9, C.L);
+  if (!(rn_add(rn_mul(rx, rx), rn_mul(ry, ry)) <= rn_mul(tolr, tolr))) return false;
+  const double l0 = rn_sub(rn_sub(1.0, xi), eta);
+  return xi >= -kBaryTol && eta >= -kBaryTol && l0 >= -kBaryTol;
+}
+
+// K1 for curved elements: overwrite the sources of the listed curved
+// elements with y_i = rho(xi_i), q_i *= |J(xi_i)| / det (k_sources used the chord)
+__global__ void k_sources_curved(int64_t n, const int32_t* __restrict__ celist, int len_q,
+                                 const ElemRec* __restrict__ el, CurvesDev CV, const RulesDev* __restrict__ R,
+                                 double* __restrict__ sx, double* __restrict__ sy, double* __restrict__ sq) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n * len_q) return;
+  const int64_t k = s / len_q;
+  const int i = (int)(s - k * len_q);
+  const int64_t e = celist[k];
+  const ElemRec& T = el[e];
+  const CurveRef C = curve_of(CV, CV.ecurve[e]);
+  double x, y, J[4];
+  blend_jac<false>(bgeom_of(T), C, R->far_x[i], R->far_y[i], x, y, J);
+  const int64_t o = e * len_q + i;
+  sx[o] = x;
+  sy[o] = y;
+  sq[o] = sq[o] * (fabs(J[0] * J[3] - J[1] * J[2]) / T.det);
+}
 
 // ---------------------------------------------------------------------------
 // K1: point sources y_i = rho_T(xi_i), q_i = w_i |J_T| f_T(xi_i) / (4 pi).
@@ -136,7 +185,7 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
                         const int32_t* __restrict__ celems, const int32_t* __restrict__ allnear,
                         int n_allnear, int32_t* __restrict__ self_out,
                         int64_t* __restrict__ cnt_out, const int64_t* __restrict__ off,
-                        int32_t* __restrict__ ids, double2* __restrict__ self_ref) {
+                        int32_t* __restrict__ ids, double2* __restrict__ self_ref, CurvesDev CV) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const double2 p = txy[t];
@@ -170,7 +219,8 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
     if ((R.ball != 0.0 || R.ta0 >= 0.0) && !(tx >= R.bx0 && tx <= R.bx1 && ty >= R.by0 && ty <= R.by1)) continue;
     if (self < 0) {
       double xi, eta;
-      if (rn_locate(R, tx, ty, xi, eta)) {
+      const int cid = curve_id_of(CV, id);
+      if (cid < 0 ? rn_locate(R, tx, ty, xi, eta) : rn_locate_curved(R, curve_of(CV, cid), tx, ty, xi, eta)) {
         self = id;
         sxi = xi;
         seta = eta;
@@ -405,7 +455,7 @@ __global__ void __launch_bounds__(128)
                   const ElemRec* __restrict__ el, const RulesDev* __restrict__ R,
                   int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
                   unsigned long long* __restrict__ leaves, unsigned long long* __restrict__ stats,
-                  int* __restrict__ err) {
+                  int* __restrict__ err, CurvesDev CV) {
   __shared__ double skd[kMaxNearDepth + 2];
   for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
@@ -413,7 +463,9 @@ __global__ void __launch_bounds__(128)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long rle1 = 0;
   int maxd = 0;
-  if (p < n_pairs) {
+  if (p < n_pairs && curve_id_of(CV, pair_elem[p]) >= 0) {
+    if (!FILL) cnt[p] = 0;  // curved element: k_near_curved
+  } else if (p < n_pairs) {
     const int32_t e = pair_elem[p];
     const double2 tp = txy[pair_tgt[p]];
     const ElemRec E = el[e];
@@ -731,7 +783,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
            const double* __restrict__ coeffs, const double* __restrict__ sx,
            const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
            const SelfTab* __restrict__ ST, double* __restrict__ corr, double* __restrict__ sub_out,
-           int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats) {
+           int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV) {
   constexpr int M = (P + 1) * (P + 2) / 2;
   constexpr int NP = P + 1, NP2 = NP * NP;
   __shared__ double scc[SELF_WARPS][M];
@@ -773,6 +825,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       }
       continue;
     }
+    if (curve_id_of(CV, e) >= 0) continue;  // curved element: k_self_curved
     const double2 tp = txy[t];
     const double tx = tp.x, ty = tp.y;
     const ElemRec& Er = el[e];
@@ -890,6 +943,280 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     my_degen = 0;
   }
   if (lane == 0 && my_degen) atomicAdd(&stats[4], my_degen);
+}
+
+// ---------------------------------------------------------------------------
+// Curved elements (oracle near_rec / self_eval_curved).
+// The pairs and self items whose element is curved skip K4/K5 and take these
+// kernels: one warp per item, the element's coefficients in shared memory.
+//  * k_near_curved: the warp walks the 4-way subdivision depth-first in
+//    lockstep (a per-warp stack of path codes in shared memory); acceptance
+//    uses the blended sub-simplex vertices and their chords with exact
+//    rounding (leaf counts match the oracle); lanes split each leaf's N_n
+//    nodes, each weighted by |J| of the blending map.
+//  * k_self_curved: sub-elements (t, gamma) and the two straight sides; the
+//    density at every (r_j, s) node through the Newton inverse of the
+//    blending map seeded on the radial line in reference coordinates.
+constexpr int CURV_WARPS = 4;
+
+template <int P>
+__global__ void __launch_bounds__(CURV_WARPS * 32)
+    k_near_curved(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
+                  const double2* __restrict__ txy, const ElemRec* __restrict__ el,
+                  const double* __restrict__ coeffs, CurvesDev CV, const double* __restrict__ sx,
+                  const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
+                  double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ lcnt,
+                  unsigned long long* __restrict__ stats, int* __restrict__ err) {
+  constexpr int M = (P + 1) * (P + 2) / 2;
+  __shared__ double scc[CURV_WARPS][M];
+  __shared__ unsigned long long sstack[CURV_WARPS][kStackCap];
+  __shared__ double skd[kMaxNearDepth + 2];
+  __shared__ double2 sltab[kLogEntries];
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
+  for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
+  __syncthreads();
+  const double ball_factor = R->near_model == 1 ? R->ball_factor : 0.0;
+  const int Ln = R->len_n, len_q = R->len_q;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long my_leaves = 0, my_rle1 = 0;
+  int my_maxd = 0;
+  for (int64_t p = (int64_t)blockIdx.x * CURV_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * CURV_WARPS) {
+    const int32_t e = pair_elem[p];
+    const int cid = curve_id_of(CV, e);
+    if (cid < 0) continue;
+    const CurveRef C = curve_of(CV, cid);
+    const ElemRec& Er = el[e];
+    const BlendGeom B = bgeom_of(Er);
+    const double2 tp = txy[pair_tgt[p]];
+    const double tx = tp.x, ty = tp.y;
+    __syncwarp();
+    for (int j = lane; j < M; j += 32) scc[wid][j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    if (lane == 0) sstack[wid][0] = 0ull;
+    __syncwarp();
+    int sp = 1;
+    bool bad = false;
+    double acc = 0.0;
+    long long nleaf = 0;
+    while (sp > 0) {
+      const unsigned long long code = sstack[wid][--sp];
+      __syncwarp();
+      const int d = (int)(code >> 58);
+      const unsigned long long path = code & kPathMask;
+      double v[6];
+      decode_path(path, d, v[0], v[1], v[2], v[3], v[4], v[5]);
+      double px[3], py[3];
+#pragma unroll 1
+      for (int k = 0; k < 3; ++k) blend<true>(B, C, v[2 * k], v[2 * k + 1], px[k], py[k]);
+      bool accept, le1 = false;
+      if (ball_factor > 0.0) {
+        accept = d >= kBallMaxDepth || !rn_ball_test(px[0], py[0], px[1], py[1], px[2], py[2], ball_factor, tx, ty);
+      } else {
+        const double rd = rn_mul(Er.rho0n, skd[d]);
+        if (!(rd > 1.0)) {
+          accept = le1 = true;
+        } else {
+          const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+          double dist[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) dist[k] = rn_dist(tx, ty, px[k], py[k]);
+          bool nearp = false;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int k1 = (k + 1) % 3;
+            const double len = rn_dist(px[k1], py[k1], px[k], py[k]);
+            if (rn_add(dist[k], dist[k1]) < rn_mul(g, len)) nearp = true;
+          }
+          accept = !nearp;
+        }
+      }
+      if (accept) {
+        ++nleaf;
+        my_rle1 += le1 ? 1ull : 0ull;
+        my_maxd = max(my_maxd, d);
+        const double scale = ldexp(1.0, -2 * d) * kInv4Pi;
+        const double bax = v[2] - v[0], bay = v[3] - v[1], cax = v[4] - v[0], cay = v[5] - v[1];
+        for (int i = lane; i < Ln; i += 32) {
+          const double u = R->near_x[i], w = R->near_y[i];
+          const double xi = v[0] + (u * bax + w * cax), eta = v[1] + (u * bay + w * cay);
+          double yx, yy, J[4];
+          blend_jac<false>(B, C, xi, eta, yx, yy, J);
+          const double jw = fabs(J[0] * J[3] - J[1] * J[2]);
+          const double f = density<P>(ShCoef(scc[wid]), xi, eta);
+          const double dx = tx - yx, dy = ty - yy;
+          acc += (R->near_w[i] * jw) * f * log(dx * dx + dy * dy) * scale;
+        }
+      } else {
+        if (d + 1 > kMaxPathDepth || sp + 4 > kStackCap) {
+          bad = true;
+          break;
+        }
+        const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
+        if (lane == 0) {
+          sstack[wid][sp] = base | 3ull;
+          sstack[wid][sp + 1] = base | 2ull;
+          sstack[wid][sp + 2] = base | 1ull;
+          sstack[wid][sp + 3] = base;
+        }
+        sp += 4;
+        __syncwarp();
+      }
+    }
+    const double val = warp_sum(acc);
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
+    if (lane == 0) {
+      corr[p] = sub_out ? val : val - sub;
+      if (sub_out) sub_out[p] = sub;
+      if (lcnt) lcnt[p] = bad ? 0 : nleaf;
+      if (bad) atomicExch(err, 2);
+      my_leaves += (unsigned long long)nleaf;
+    }
+  }
+  if (lane == 0) {
+    if (my_leaves) atomicAdd(&stats[6], my_leaves);
+    if (my_rle1) atomicAdd(&stats[1], my_rle1);
+    if (my_maxd) atomicMax(&stats[2], (unsigned long long)my_maxd);
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(CURV_WARPS * 32)
+    k_self_curved(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
+                  const double2* __restrict__ txy, const ElemRec* __restrict__ el,
+                  const double* __restrict__ coeffs, CurvesDev CV, const double* __restrict__ sx,
+                  const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
+                  double* __restrict__ corr, double* __restrict__ sub_out, int64_t* __restrict__ panels_out,
+                  unsigned long long* __restrict__ stats) {
+  constexpr int M = (P + 1) * (P + 2) / 2;
+  __shared__ double scc[CURV_WARPS][M];
+  __shared__ double sglx[kMaxGL], sglw[kMaxGL], sgr[kMaxGGQ], sgw[kMaxGGQ], sglr[kMaxGGQ];
+  __shared__ double2 sltab[kLogEntries];
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
+  const int NL = R->n_l, NG = R->n_g1, len_q = R->len_q;
+  for (int i = threadIdx.x; i < NL; i += blockDim.x) {
+    sglx[i] = R->gl_x[i];
+    sglw[i] = R->gl_w[i];
+  }
+  for (int i = threadIdx.x; i < NG; i += blockDim.x) {
+    sgr[i] = R->ggq_r[i];
+    sgw[i] = R->ggq_w[i] * R->ggq_r[i];
+    sglr[i] = R->ggq_lr[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long my_panels = 0, my_degen = 0;
+  for (int64_t it = (int64_t)blockIdx.x * CURV_WARPS + wid; it < n_items; it += (int64_t)gridDim.x * CURV_WARPS) {
+    const int32_t t = item_tgt ? item_tgt[it] : (int32_t)it;
+    const int32_t e = item_elem[it];
+    if (e < 0) continue;
+    const int cid = curve_id_of(CV, e);
+    if (cid < 0) continue;
+    const CurveRef C = curve_of(CV, cid);
+    const ElemRec& Er = el[e];
+    const BlendGeom B = bgeom_of(Er);
+    const double2 tp = txy[t];
+    const double tx = tp.x, ty = tp.y;
+    double txi, teta;
+    rn_locate_curved(Er, C, tx, ty, txi, teta);
+    __syncwarp();
+    for (int j = lane; j < M; j += 32) scc[wid][j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    __syncwarp();
+    double acc = 0.0;
+    long long npan_item = 0;
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      const bool arc = k == 0;
+      SelfGeom G;
+      double grA_x = 0.0, grA_y = 0.0, grB_x = 0.0, grB_y = 0.0;
+      if (arc) {
+        G.L = C.L;
+        G.st = curved_argmin<true>(C, tx, ty);
+        double gx, gy;
+        curve_eval<true>(C, rn_sub(1.0, G.st / G.L), gx, gy);
+        // t on the arc: the sub-element (t, gamma) keeps its area; panels
+        // refine down to 1e-9 L (oracle self_eval_curved)
+        double dmin = rn_dist(tx, ty, gx, gy);
+        if (!(dmin > rn_mul(1e-13, G.L))) dmin = rn_mul(1e-9, G.L);
+        G.degenerate = false;
+        int N = 0;
+        for (double x = G.st; !(x < dmin) && N < 1100; x *= 0.5) ++N;
+        int Mr = 0;
+        for (double x = rn_sub(G.L, G.st); !(x < dmin) && Mr < 1100; x *= 0.5) ++Mr;
+        G.N = N;
+        G.Mr = Mr;
+        G.npan = N + Mr + 2;
+        G.h = 0.0;
+      } else {
+        // straight sides (v1, v2) and (v2, v0); reference corners (1,0), (0,1), (0,0)
+        const double Ax = k == 1 ? Er.x1 : Er.x2, Ay = k == 1 ? Er.y1 : Er.y2;
+        const double Bx = k == 1 ? Er.x2 : Er.x0, By = k == 1 ? Er.y2 : Er.y0;
+        self_geom(tx, ty, Ax, Ay, Bx, By, G);
+        grA_x = k == 1 ? 1.0 : 0.0;
+        grA_y = k == 1 ? 0.0 : 1.0;
+        grB_x = 0.0;
+        grB_y = k == 1 ? 1.0 : 0.0;
+      }
+      if (G.degenerate) {
+        ++my_degen;
+        continue;
+      }
+      const int nodes = G.npan * NL;
+      for (int j = lane; j < nodes; j += 32) {
+        const int pi = j / NL, gq = j - pi * NL;
+        const double s0 = self_bnd(G, pi), s1 = self_bnd(G, pi + 1);
+        if (!(s1 > s0)) continue;
+        const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
+        const double s = mid + half * sglx[gq];
+        const double ws = half * sglw[gq];
+        const double sl = s / G.L;
+        double px, py, jf, grx, gry;
+        if (arc) {
+          double g[2], g1[2], g2[2];
+          curve_eval_d<false>(C, 1.0 - sl, g, g1, g2);
+          px = g[0];
+          py = g[1];
+          const double tgx = -g1[0] / G.L, tgy = -g1[1] / G.L;
+          jf = fabs((px - tx) * tgy - (py - ty) * tgx);
+          grx = sl;
+          gry = 0.0;
+        } else {
+          px = G.Ax + sl * G.ABx;
+          py = G.Ay + sl * G.ABy;
+          jf = G.h;
+          grx = grA_x + sl * (grB_x - grA_x);
+          gry = grA_y + sl * (grB_y - grA_y);
+        }
+        const double ddx = px - tx, ddy = py - ty;
+        const double lr0 = 0.5 * log(ddx * ddx + ddy * ddy);
+        double inner = 0.0;
+        for (int jg = 0; jg < NG; ++jg) {
+          const double rj = sgr[jg];
+          const double yx = tx + rj * (px - tx), yy = ty + rj * (py - ty);
+          double xi = txi + rj * (grx - txi), eta = teta + rj * (gry - teta);
+          blend_inverse_tol(B, C, yx, yy, xi, eta);
+          const double xc = fmin(fmax(xi, 0.0), 1.0);
+          const double ec = fmin(fmax(eta, 0.0), 1.0 - xc);
+          const double f = density<P>(ShCoef(scc[wid]), xc, ec);
+          inner += sgw[jg] * (lr0 + sglr[jg]) * f;
+        }
+        acc += ws * jf * inner;
+      }
+      for (int pi = 0; pi < G.npan; ++pi)
+        if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
+    }
+    const double val = warp_sum(acc) * kInv2Pi;
+    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
+    if (lane == 0) {
+      corr[it] = sub_out ? val : val - sub;
+      if (sub_out) sub_out[it] = sub;
+      if (panels_out) panels_out[it] = npan_item;
+      my_panels += (unsigned long long)npan_item;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (my_panels) atomicAdd(&stats[3], my_panels);
+    if (my_degen) atomicAdd(&stats[4], my_degen);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1130,6 +1457,11 @@ struct vp_ctx {
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
+  // curved (blending-map) elements, SURVEY.md §8(f3)
+  int curve_deg = 0;
+  std::vector<int32_t> h_ecurve, h_celist;
+  std::vector<double> h_ccx, h_ccy, h_clen;
+  DevBuf d_ecurve, d_ccx, d_ccy, d_clen, d_celist;
 };
 
 namespace {
@@ -1147,6 +1479,19 @@ int set_err(vp_ctx* c, int code, const std::string& m) {
   } while (0)
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+bool has_curves(const vp_ctx* c) { return !c->h_celist.empty(); }
+CurvesDev curves_dev(const vp_ctx* c) {
+  CurvesDev cv{};
+  if (has_curves(c)) {
+    cv.ecurve = c->d_ecurve.as<int32_t>();
+    cv.cx = c->d_ccx.as<double>();
+    cv.cy = c->d_ccy.as<double>();
+    cv.len = c->d_clen.as<double>();
+    cv.D = c->curve_deg;
+  }
+  return cv;
+}
 
 // Per-element records on the host with the oracle's operation order
 // (oracle/vp_oracle.cpp Setup::init): list predicates stay bit-exact.
@@ -1227,6 +1572,18 @@ int build_elements(vp_ctx* c) {
       const double rr = ta[k] * 0.5 * (1.0 + 1e-9) + 1e-300;
       lox = std::min(lox, mx - rr); hix = std::max(hix, mx + rr);
       loy = std::min(loy, my - rr); hiy = std::max(hiy, my + rr);
+    }
+    if (!c->h_ecurve.empty() && c->h_ecurve[e] >= 0) {  // the element bulges past its chord
+      const int cid = c->h_ecurve[e], D = c->curve_deg;
+      const CurveRef C{c->h_ccx.data() + (int64_t)cid * (D + 1), c->h_ccy.data() + (int64_t)cid * (D + 1), D,
+                       c->h_clen[cid]};
+      for (int k = 0; k <= 32; ++k) {
+        double gx, gy;
+        curve_eval<true>(C, k / 32.0, gx, gy);
+        const double pad = 1e-9 * C.L + 1e-300;
+        lox = std::min(lox, gx - 0.05 * C.L - pad); hix = std::max(hix, gx + 0.05 * C.L + pad);
+        loy = std::min(loy, gy - 0.05 * C.L - pad); hiy = std::max(hiy, gy + 0.05 * C.L + pad);
+      }
     }
     R.ta0 = ta[0]; R.ta1 = ta[1]; R.ta2 = ta[2];
     R.bx0 = lox; R.by0 = loy; R.bx1 = hix; R.by1 = hiy;
@@ -1337,6 +1694,16 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
                                                      c->d_nps.as<double>(), corr, sub);
 }
 
+template <int P>
+void launch_near_curved(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
+                        double* corr, double* sub) {
+  const int blocks = (int)std::min<int64_t>(nblk(n, CURV_WARPS), (int64_t)c->sm_count * 16);
+  k_near_curved<P><<<std::max(blocks, 1), CURV_WARPS * 32, 0, c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), curves_dev(c), c->d_sx.as<double>(),
+      c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, c->d_lcnt.as<int64_t>(),
+      c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+}
+
 int build_near_cache(vp_ctx* c);
 
 int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
@@ -1345,7 +1712,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_loff.ensure(sizeof(int64_t) * (n + 1)));
   k_near_leaves<false><<<nblk(n, 128), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), nullptr,
-      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c));
   CUDA_TRY(c, cudaMemsetAsync(c->d_lcnt.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1, c->stream);
@@ -1359,12 +1726,17 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_leafcodes.ensure(sizeof(unsigned long long) * (nleaves + 1)));
   k_near_leaves<true><<<nblk(n, 128), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
-      c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
+      c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>(),
+      curves_dev(c));
   if (int rc = build_near_cache(c)) return rc;
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
   VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub);
+  if (has_curves(c)) {
+    VP_DISPATCH_P(c->p, launch_near_curved, c, n, ptgt, pelem, txy, corr, sub);
+    c->last_launches += 1;
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->n_leaves_last = nleaves;
   c->last_launches += 7;
@@ -1380,7 +1752,15 @@ void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem
   k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
       c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
-      sub, panels, c->d_stats.as<unsigned long long>());
+      sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c));
+  if (has_curves(c)) {
+    const int cb = (int)std::min<int64_t>(nblk(n, CURV_WARPS), (int64_t)c->sm_count * 16);
+    k_self_curved<P><<<std::max(cb, 1), CURV_WARPS * 32, 0, c->stream>>>(
+        n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), curves_dev(c), c->d_sx.as<double>(),
+        c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
+        c->d_stats.as<unsigned long long>());
+    c->last_launches += 1;
+  }
 }
 
 
@@ -1509,6 +1889,13 @@ int compute_sources(vp_ctx* c) {
                                                   c->d_coeffs.as<double>(), c->d_V.as<double>(),
                                                   c->d_rules.as<RulesDev>(), c->d_sx.as<double>(),
                                                   c->d_sy.as<double>(), c->d_sq.as<double>());
+  if (has_curves(c)) {
+    const int64_t nc = (int64_t)c->h_celist.size();
+    k_sources_curved<<<nblk(nc * c->rules.len_q, 128), 128, 0, c->stream>>>(
+        nc, c->d_celist.as<int32_t>(), c->rules.len_q, c->d_el.as<ElemRec>(), curves_dev(c),
+        c->d_rules.as<RulesDev>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>());
+    c->last_launches += 1;
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->sources_valid = true;
   c->last_launches += 1;
@@ -1674,7 +2061,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   k_lists<false><<<nblk(T, 128), 128, 0, c->stream>>>(
       T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
-      c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>());
+      c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c));
   CUDA_TRY(c, cudaMemsetAsync(c->d_cnt.as<int64_t>() + T, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
@@ -1687,7 +2074,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   k_lists<true><<<nblk(T, 128), 128, 0, c->stream>>>(
       T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr,
-      c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), nullptr);
+      c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), nullptr, curves_dev(c));
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 3;
   *n_ids_out = n_ids;
@@ -1742,7 +2129,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     std::memset(st, 0, sizeof(*st));
     st->n_targets = T;
     st->n_near_pairs = n_ids;
-    st->n_leaves = n_ids > 0 ? c->n_leaves_last : 0;
+    st->n_leaves = (n_ids > 0 ? c->n_leaves_last : 0) + (int64_t)hs[6];
     st->n_rho_le1 = (int64_t)hs[1];
     st->max_depth = (int32_t)hs[2];
     st->n_panels = (int64_t)hs[3];
@@ -1908,6 +2295,8 @@ int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, con
   c->n_vert = n_vert;
   c->n_tri = n_tri;
   c->have_mesh = true;
+  c->h_ecurve.clear();
+  c->h_celist.clear();
   c->sources_valid = false;
   // triangle orientation is validated here so errors surface early
   for (int64_t e = 0; e < n_tri; ++e) {
@@ -1925,6 +2314,59 @@ int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, con
     if (int rc = build_elements(c)) return rc;
   }
   if (c->have_density && c->M > 0) c->have_density = false;  // coefficients are per triangle
+  return 0;
+}
+
+int vp_set_curves(vp_ctx* c, const int32_t* curve_id, int deg, int64_t n_curves, const double* cx,
+                  const double* cy, const double* len) {
+  if (!c) return 1;
+  if (!c->have_mesh) return set_err(c, 1, "set_curves: call vp_set_mesh first");
+  c->h_ecurve.clear();
+  c->h_celist.clear();
+  c->sources_valid = false;
+  if (curve_id) {
+    if (deg < 1 || deg > 64) return set_err(c, 1, "set_curves: degree must be in [1, 64]");
+    if (n_curves <= 0 || !cx || !cy || !len) return set_err(c, 1, "set_curves: empty curve arrays");
+    for (int64_t i = 0; i < n_curves; ++i)
+      if (!(len[i] > 0.0) || !std::isfinite(len[i])) return set_err(c, 1, "set_curves: arc length must be > 0");
+    for (int64_t i = 0; i < n_curves * (deg + 1); ++i)
+      if (!std::isfinite(cx[i]) || !std::isfinite(cy[i])) return set_err(c, 2, "set_curves: non-finite coefficient");
+    std::vector<int32_t> ec(curve_id, curve_id + c->n_tri);
+    std::vector<int32_t> cl;
+    for (int64_t e = 0; e < c->n_tri; ++e) {
+      if (ec[e] < -1 || ec[e] >= n_curves) return set_err(c, 1, "set_curves: curve id out of range");
+      if (ec[e] >= 0) cl.push_back((int32_t)e);
+    }
+    if (!cl.empty()) {
+      c->curve_deg = deg;
+      c->h_ecurve = std::move(ec);
+      c->h_celist = std::move(cl);
+      c->h_ccx.assign(cx, cx + n_curves * (deg + 1));
+      c->h_ccy.assign(cy, cy + n_curves * (deg + 1));
+      c->h_clen.assign(len, len + n_curves);
+      CUDA_TRY(c, cudaSetDevice(c->device));
+      CUDA_TRY(c, c->d_ecurve.ensure(sizeof(int32_t) * c->n_tri));
+      CUDA_TRY(c, c->d_celist.ensure(sizeof(int32_t) * c->h_celist.size()));
+      CUDA_TRY(c, c->d_ccx.ensure(sizeof(double) * c->h_ccx.size()));
+      CUDA_TRY(c, c->d_ccy.ensure(sizeof(double) * c->h_ccy.size()));
+      CUDA_TRY(c, c->d_clen.ensure(sizeof(double) * n_curves));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_ecurve.p, c->h_ecurve.data(), sizeof(int32_t) * c->n_tri,
+                                  cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_celist.p, c->h_celist.data(), sizeof(int32_t) * c->h_celist.size(),
+                                  cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_ccx.p, c->h_ccx.data(), sizeof(double) * c->h_ccx.size(),
+                                  cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_ccy.p, c->h_ccy.data(), sizeof(double) * c->h_ccy.size(),
+                                  cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_clen.p, c->h_clen.data(), sizeof(double) * n_curves, cudaMemcpyHostToDevice,
+                                  c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  if (c->have_rules) {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (int rc = build_elements(c)) return rc;
+  }
   return 0;
 }
 

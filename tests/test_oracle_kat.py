@@ -245,6 +245,8 @@ def test_curved_disk_constant_density_is_exact():
     """f = 1 on the exact unit disk: u = (|x|^2 - 1)/4.  The polygonal mesh
     misses it by its O(h^2) domain error; blended boundary elements reach eps."""
     pr, sub = _disk_sample()
+    th = np.linspace(0.1, 6.0, 13)  # targets on the arcs themselves
+    sub = np.concatenate([sub, np.stack([np.cos(th), np.sin(th)], 1)])
     tri, cv = vp.curve_boundary_of_disk(pr.vxy, pr.tri)
     assert (cv.curve_id >= 0).sum() == 256
     co = const_coeffs(len(tri), pr.p)
