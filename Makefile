@@ -11,14 +11,18 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -v 
 CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(CSRC)
 
 LIB := $(PKG)/libvp_b200.so
-OBJS := $(CSRC)/vp_b200.o $(CSRC)/vp_setup.o
+OBJS := $(CSRC)/vp_b200.o $(CSRC)/vp_setup.o $(CSRC)/vp_curves.o
 
 all: $(LIB) oracle
 
-$(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/koorn.cuh include/vp.h
+$(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/vp_curve.cuh $(CSRC)/vp_fmm.cuh \
+		$(CSRC)/koorn.cuh include/vp.h include/vp_setup.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; exit 1)
 
 $(CSRC)/vp_setup.o: $(CSRC)/vp_setup.cpp $(CSRC)/koorn.cuh include/vp_setup.h
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(CSRC)/vp_curves.o: $(CSRC)/vp_curves.cpp include/vp_setup.h
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)

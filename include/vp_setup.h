@@ -48,6 +48,38 @@ int vps_ggq(int ng, double* r, double* w, double* max_residual);
 int vps_circle_arc(double cx, double cy, double R, double th0, double th1, int deg, double* gx, double* gy,
                    double* len);
 
+/* Closed boundary curves with arc-length parametrisation (the reference's
+ * curve layer, curve.hpp:16-332: ParamCurve kinds + ArcLengthCurve), used to
+ * build the per-element Legendre series of vp_set_curves (SPEC.md:200-210
+ * annotate_boundary).  Parameter t in [0, 1]; arc length s in [0, L). */
+typedef struct vps_curve vps_curve;
+enum {
+  VPS_CURVE_CIRCLE = 0,  /* (cx, cy, r): c + r (cos 2 pi t, sin 2 pi t)        curve.hpp:25-45 */
+  VPS_CURVE_ELLIPSE = 1, /* (a, b): (a cos 2 pi t, b sin 2 pi t)                curve.hpp:47-67 */
+  VPS_CURVE_WOBBLY = 2,  /* (a, b, k): polar r = a + b cos(k theta), a > |b|    curve.hpp:69-101 */
+  VPS_CURVE_HERMITE = 3, /* n x (t, x, y, dx, dy): periodic cubic Hermite       curve.hpp:103-162 */
+  VPS_CURVE_ARC = 4      /* (cx, cy, r, th0, th1): closed only if |th1-th0| = 2 pi */
+};
+/* Errors: 1 with "reparametrize: curve is not closed" when |gamma(0) -
+ * gamma(1)| > 1e-8 L (curve.hpp:250-252); Hermite parameter checks as
+ * curve.hpp:108-116. */
+int vps_curve_create(int kind, const double* params, int n_params, vps_curve** out);
+void vps_curve_destroy(vps_curve* c);
+double vps_curve_length(const vps_curve* c);
+int vps_curve_ccw(const vps_curve* c);
+/* s -> t (the arc-length inverse) */
+int vps_curve_param(const vps_curve* c, double s, double* t);
+/* Gamma(s), unit tangent Gamma'(s) and Gamma''(s) at n arc lengths (s wraps
+ * modulo L); tangent/dd may be NULL */
+int vps_curve_points(const vps_curve* c, int64_t n, const double* s, double* xy, double* tangent, double* dd);
+/* closest point: s and distance for n points (sdf.hpp:56-80 closest_point) */
+int vps_curve_closest(const vps_curve* c, int64_t n, const double* xy, double* s, double* dist);
+/* G(tau) = Gamma(s_from + tau (s_to - s_from)), tau in [0,1], as a degree-deg
+ * Legendre series in P_n(2 tau - 1); *len = |s_to - s_from| */
+int vps_curve_segment(const vps_curve* c, double s_from, double s_to, int deg, double* gx, double* gy,
+                      double* len);
+const char* vps_curve_last_error(void);
+
 /* Target nodes on the reference simplex: shifted principal lattice
  * ((i+1)/(p+3), (j+1)/(p+3)), i+j <= p; (p+1)(p+2)/2 nodes. */
 int vps_lattice_nodes(int p, double* x, double* y);

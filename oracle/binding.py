@@ -102,7 +102,8 @@ def ref():
         R.vpref_koornwinder.argtypes = [i32, dbl, dbl, _d_p]
         R.vpref_gauss_legendre.argtypes = [i32, _d_p, _d_p]
         R.vpref_quadtree_query.argtypes = [i64, _d_p, i32, dbl, dbl, dbl, dbl, _i32_p, i64, _i64_p, _i64_p]
-        for f in (R.vpref_koornwinder, R.vpref_gauss_legendre, R.vpref_quadtree_query):
+        R.vpref_arclength.argtypes = [i32, _d_p, i32, i64, _d_p, _d_p, _d_p, _d_p, _d_p, ctypes.POINTER(i32)]
+        for f in (R.vpref_koornwinder, R.vpref_gauss_legendre, R.vpref_quadtree_query, R.vpref_arclength):
             f.restype = i32
         _ref = R
     return _ref
@@ -259,3 +260,20 @@ def ref_gauss_legendre(n):
     if rc:
         raise OracleError(rc, "reference gauss_legendre failed")
     return x, w
+
+
+def ref_arclength(kind, params, s):
+    """The reference's ArcLengthCurve (curve.hpp:184-332) at arc lengths s:
+    (xy, tangent, d2/ds2, length, ccw)."""
+    R = ref()
+    if R is None:
+        raise OracleError(1, "oracle/_ref not built")
+    prm = np.ascontiguousarray(params, dtype=np.float64).ravel()
+    s = np.ascontiguousarray(np.atleast_1d(s), dtype=np.float64)
+    xy, tg, dd = np.zeros((s.size, 2)), np.zeros((s.size, 2)), np.zeros((s.size, 2))
+    ln, ccw = ctypes.c_double(), ctypes.c_int()
+    rc = R.vpref_arclength(kind, _d(prm), prm.size, s.size, _d(s), _d(xy), _d(tg), _d(dd), ctypes.byref(ln),
+                           ctypes.byref(ccw))
+    if rc != 0:
+        raise OracleError(rc, "reference reparametrize failed")
+    return xy, tg, dd, ln.value, bool(ccw.value)

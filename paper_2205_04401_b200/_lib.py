@@ -101,6 +101,17 @@ _SIGS = [
     ("vps_ggq", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p, c_double_p]),
     ("vps_circle_arc", ctypes.c_int, [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_int, c_double_p, c_double_p, c_double_p]),
+    ("vps_curve_create", ctypes.c_int, [ctypes.c_int, c_double_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    ("vps_curve_destroy", None, [ctypes.c_void_p]),
+    ("vps_curve_length", ctypes.c_double, [ctypes.c_void_p]),
+    ("vps_curve_ccw", ctypes.c_int, [ctypes.c_void_p]),
+    ("vps_curve_param", ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, c_double_p]),
+    ("vps_curve_points", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_double_p, c_double_p,
+                                        c_double_p]),
+    ("vps_curve_closest", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_double_p, c_double_p]),
+    ("vps_curve_segment", ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                         c_double_p, c_double_p, c_double_p]),
+    ("vps_curve_last_error", ctypes.c_char_p, []),
     ("vps_lattice_nodes", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p]),
     ("vps_density_eval", ctypes.c_double, [ctypes.c_int, c_double_p, ctypes.c_int, ctypes.c_double,
                                            ctypes.c_double]),

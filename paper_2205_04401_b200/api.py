@@ -255,6 +255,165 @@ def circle_arc(cx, cy, R, th0, th1, deg=16):
     return gx, gy, ln.value
 
 
+class BoundaryCurve:
+    """Closed boundary curve with its arc-length parametrisation (the
+    reference's ParamCurve + ArcLengthCurve, curve.hpp:16-332), host C++."""
+
+    CIRCLE, ELLIPSE, WOBBLY, HERMITE, ARC = 0, 1, 2, 3, 4
+
+    def __init__(self, kind, params):
+        self._L = _lib.lib()
+        prm = np.ascontiguousarray(params, dtype=np.float64).ravel()
+        h = ctypes.c_void_p()
+        _check(self._L.vps_curve_create(kind, _d(prm), prm.size, ctypes.byref(h)),
+               self._L.vps_curve_last_error().decode())
+        self._h = h
+        self.kind = kind
+        self.length = self._L.vps_curve_length(h)
+        self.ccw = bool(self._L.vps_curve_ccw(h))
+
+    @classmethod
+    def circle(cls, cx=0.0, cy=0.0, r=1.0):
+        return cls(cls.CIRCLE, [cx, cy, r])
+
+    @classmethod
+    def ellipse(cls, a, b):
+        return cls(cls.ELLIPSE, [a, b])
+
+    @classmethod
+    def wobbly(cls, a, b, k):
+        return cls(cls.WOBBLY, [a, b, k])
+
+    @classmethod
+    def hermite(cls, samples):
+        """samples: rows `t x y dx dy` (the reference's curve text format)."""
+        return cls(cls.HERMITE, np.asarray(samples, dtype=np.float64).reshape(-1, 5))
+
+    @classmethod
+    def arc(cls, cx, cy, r, th0, th1):
+        return cls(cls.ARC, [cx, cy, r, th0, th1])
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._L.vps_curve_destroy(self._h)
+            self._h = None
+
+    def param(self, s):
+        t = ctypes.c_double()
+        _check(self._L.vps_curve_param(self._h, float(s), ctypes.byref(t)), self._L.vps_curve_last_error().decode())
+        return t.value
+
+    def points(self, s):
+        """(Gamma(s), unit tangent, Gamma''(s)) at arc lengths s."""
+        s = np.ascontiguousarray(np.atleast_1d(s), dtype=np.float64)
+        xy, tg, dd = np.zeros((s.size, 2)), np.zeros((s.size, 2)), np.zeros((s.size, 2))
+        _check(self._L.vps_curve_points(self._h, s.size, _d(s), _d(xy), _d(tg), _d(dd)),
+               self._L.vps_curve_last_error().decode())
+        return xy, tg, dd
+
+    def closest(self, xy):
+        xy = _f64(xy, (-1, 2))
+        s, dist = np.zeros(xy.shape[0]), np.zeros(xy.shape[0])
+        _check(self._L.vps_curve_closest(self._h, xy.shape[0], _d(xy), _d(s), _d(dist)),
+               self._L.vps_curve_last_error().decode())
+        return s, dist
+
+    def segment(self, s_from, s_to, deg=16):
+        gx, gy, ln = np.zeros(deg + 1), np.zeros(deg + 1), ctypes.c_double()
+        _check(self._L.vps_curve_segment(self._h, float(s_from), float(s_to), deg, _d(gx), _d(gy), ctypes.byref(ln)),
+               self._L.vps_curve_last_error().decode())
+        return gx, gy, ln.value
+
+
+def curves_from_annotation(vxy, tri, meta, curves, deg=16):
+    """Curved elements from the reference's TriMesh annotation (SPEC.md:171,
+    mesh file `e i j k kind opp curve s_a s_b`): meta rows (kind, opp, curve,
+    s_a, s_b), kind 0 straight.  Returns (tri reordered to (gamma(L), gamma(0),
+    O) for curved elements, Curves)."""
+    vxy = np.asarray(vxy, dtype=np.float64)
+    tri = np.array(tri, dtype=np.int32).reshape(-1, 3).copy()
+    cid = -np.ones(len(tri), dtype=np.int32)
+    cxs, cys, lens = [], [], []
+    for e, row in enumerate(meta):
+        kind, opp, ci, sa, sb = int(row[0]), int(row[1]), int(row[2]), float(row[3]), float(row[4])
+        if kind == 0:
+            continue
+        C = curves[ci]
+        o = tri[e, opp]
+        a, b = tri[e, (opp + 1) % 3], tri[e, (opp + 2) % 3]
+        if sb <= sa:
+            sb += C.length
+        pa, pb = C.points([sa, sb])[0]
+        # which stored vertex is gamma(s_a)
+        if np.hypot(*(vxy[a] - pa)) + np.hypot(*(vxy[b] - pb)) > np.hypot(*(vxy[b] - pa)) + np.hypot(*(vxy[a] - pb)):
+            a, b = b, a
+        if max(np.hypot(*(vxy[a] - pa)), np.hypot(*(vxy[b] - pb))) > 1e-10 * max(1.0, C.length):
+            raise UsageError(f"element {e}: curved side endpoints differ from gamma(s_a), gamma(s_b) by > 1e-10")
+        det = (vxy[b, 0] - vxy[a, 0]) * (vxy[o, 1] - vxy[a, 1]) - (vxy[o, 0] - vxy[a, 0]) * (vxy[b, 1] - vxy[a, 1])
+        if det > 0:  # (Gamma(s_a), Gamma(s_b), O) counter-clockwise: gamma(sigma) = Gamma(s_b - sigma)
+            tri[e] = (a, b, o)
+            gx, gy, ln = C.segment(sb, sa, deg)
+        else:
+            tri[e] = (b, a, o)
+            gx, gy, ln = C.segment(sa, sb, deg)
+        cid[e] = len(lens)
+        cxs.append(gx)
+        cys.append(gy)
+        lens.append(ln)
+    if not lens:
+        return tri, None
+    return tri, Curves(cid, deg, np.array(cxs), np.array(cys), np.array(lens))
+
+
+def annotate_boundary(vxy, tri, curves, tol=1e-10):
+    """annotate_boundary: every boundary edge (an edge of
+    exactly one triangle) becomes the curved side of its triangle, its
+    endpoints resolved on the nearest curve by closest point.  Returns
+    (meta rows (kind, opp, curve, s_a, s_b), vxy with the boundary vertices
+    snapped onto the curves)."""
+    vxy = np.array(vxy, dtype=np.float64).reshape(-1, 2)
+    tri = np.asarray(tri, dtype=np.int64).reshape(-1, 3)
+    edges = {}
+    for e, t in enumerate(tri):
+        for k in range(3):
+            a, b = int(t[(k + 1) % 3]), int(t[(k + 2) % 3])
+            edges.setdefault((min(a, b), max(a, b)), []).append((e, k))
+    bnd = sorted({v for (a, b), els in edges.items() if len(els) == 1 for v in (a, b)})
+    bv = np.array(bnd, dtype=np.int64)
+    best_c = np.full(len(bv), -1)
+    best_s = np.zeros(len(bv))
+    best_d = np.full(len(bv), np.inf)
+    for ci, C in enumerate(curves):
+        s, d = C.closest(vxy[bv])
+        upd = d < best_d
+        best_c[upd], best_s[upd], best_d[upd] = ci, s[upd], d[upd]
+    scale = max(max(C.length for C in curves), 1.0)
+    if (best_d > tol * scale).any():
+        raise UsageError("annotate_boundary: boundary vertex farther than tol from every curve")
+    vc = dict(zip(bnd, best_c))
+    vs = dict(zip(bnd, best_s))
+    for ci, C in enumerate(curves):
+        sel = best_c == ci
+        if sel.any():
+            vxy[bv[sel]] = C.points(best_s[sel])[0]
+    meta = np.zeros((len(tri), 5))
+    for (a, b), els in edges.items():
+        if len(els) != 1:
+            continue
+        e, k = els[0]
+        if meta[e, 0] != 0:
+            raise UsageError(f"annotate_boundary: element {e} has two boundary edges")
+        if vc[a] != vc[b]:
+            raise UsageError("annotate_boundary: boundary edge whose endpoints resolve to different curves")
+        C = curves[vc[a]]
+        sa, sb = vs[a], vs[b]
+        d = (sb - sa) % C.length
+        if d > C.length / 2:  # the short way round: s_a -> s_b increasing
+            sa, sb = sb, sa
+        meta[e] = (1, k, vc[a], sa, sb)
+    return meta, vxy
+
+
 def curve_boundary_of_disk(vxy, tri, R=1.0, deg=16, tol=1e-12):
     """Turn every triangle of a disk mesh with an edge on |x| = R into a
     curved element on the exact circle (vertices reordered to

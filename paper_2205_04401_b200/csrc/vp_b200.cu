@@ -1188,11 +1188,18 @@ __global__ void __launch_bounds__(CURV_WARPS * 32)
         const double ddx = px - tx, ddy = py - ty;
         const double lr0 = 0.5 * log(ddx * ddx + ddy * ddy);
         double inner = 0.0;
-        for (int jg = 0; jg < NG; ++jg) {
+        // rays from t: the preimage of t + r (p - t) is seeded by extrapolating
+        // the previous node's preimage along the ray from (txi, teta)
+        double pxi = grx, peta = gry, pr = 1.0;
+        for (int jg = NG - 1; jg >= 0; --jg) {
           const double rj = sgr[jg];
           const double yx = tx + rj * (px - tx), yy = ty + rj * (py - ty);
-          double xi = txi + rj * (grx - txi), eta = teta + rj * (gry - teta);
-          blend_inverse_tol(B, C, yx, yy, xi, eta);
+          const double fr = rj / pr;
+          double xi = txi + fr * (pxi - txi), eta = teta + fr * (peta - teta);
+          blend_inverse_tol(B, C, yx, yy, xi, eta, 1e-11);
+          pxi = xi;
+          peta = eta;
+          pr = rj;
           const double xc = fmin(fmax(xi, 0.0), 1.0);
           const double ec = fmin(fmax(eta, 0.0), 1.0 - xc);
           const double f = density<P>(ShCoef(scc[wid]), xc, ec);
@@ -2205,8 +2212,15 @@ int vp_create(int device, vp_ctx** out) {
   }
   double2 lt[kLogEntries];
   log_table_fill(lt);
+  double la[kMaxCurveDeg + 1], lb[kMaxCurveDeg + 1];
+  for (int k = 0; k <= kMaxCurveDeg; ++k) {
+    la[k] = leg_la(k);
+    lb[k] = leg_lb(k);
+  }
   if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
-      cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess) {
+      cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_leg_la, la, sizeof(la)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_leg_lb, lb, sizeof(lb)) != cudaSuccess) {
     vp_destroy(c);
     return 3;
   }

@@ -63,6 +63,22 @@ __host__ __device__ __forceinline__ double c_sqrt(double a) {
 #endif
 }
 
+// Legendre recurrence P_{n+1} = la_n x P_n - lb_n P_{n-1}, la_n = (2n+1)/(n+1),
+// lb_n = n/(n+1): the X = false paths multiply instead of dividing
+constexpr int kMaxCurveDeg = 64;
+__host__ __device__ __forceinline__ double leg_la(int n) { return (double)(2 * n + 1) / (double)(n + 1); }
+__host__ __device__ __forceinline__ double leg_lb(int n) { return (double)n / (double)(n + 1); }
+#ifdef __CUDACC__
+__constant__ double c_leg_la[kMaxCurveDeg + 1], c_leg_lb[kMaxCurveDeg + 1];
+#endif
+__host__ __device__ __forceinline__ double p_next(int n, double x, double p1, double p0) {
+#ifdef __CUDA_ARCH__
+  return fma(c_leg_la[n] * x, p1, -c_leg_lb[n] * p0);
+#else
+  return leg_la(n) * x * p1 - leg_lb(n) * p0;
+#endif
+}
+
 template <bool X>
 __host__ __device__ inline void curve_eval(const CurveRef& C, double tau, double& gx, double& gy) {
   const double x = c_sub<X>(c_mul<X>(2.0, tau), 1.0);
@@ -74,10 +90,15 @@ __host__ __device__ inline void curve_eval(const CurveRef& C, double tau, double
     gy = c_add<X>(gy, c_mul<X>(C.cy[1], x));
   }
   for (int n = 1; n < C.D; ++n) {
-    const double a = c_mul<X>((double)(2 * n + 1), x);
-    const double b = c_mul<X>(a, p1);
-    const double c = c_mul<X>((double)n, p0);
-    const double p2 = c_div(c_sub<X>(b, c), (double)(n + 1));
+    double p2;
+    if constexpr (X) {
+      const double a = c_mul<X>((double)(2 * n + 1), x);
+      const double b = c_mul<X>(a, p1);
+      const double c = c_mul<X>((double)n, p0);
+      p2 = c_div(c_sub<X>(b, c), (double)(n + 1));
+    } else {
+      p2 = p_next(n, x, p1, p0);
+    }
     gx = c_add<X>(gx, c_mul<X>(C.cx[n + 1], p2));
     gy = c_add<X>(gy, c_mul<X>(C.cy[n + 1], p2));
     p0 = p1;
@@ -102,8 +123,13 @@ __host__ __device__ inline void curve_eval_d(const CurveRef& C, double tau, doub
   }
   for (int n = 1; n < C.D; ++n) {
     const double k2 = (double)(2 * n + 1);
-    const double a = c_mul<X>(k2, x);
-    const double p2 = c_div(c_sub<X>(c_mul<X>(a, p1), c_mul<X>((double)n, p0)), (double)(n + 1));
+    double p2;
+    if constexpr (X) {
+      const double a = c_mul<X>(k2, x);
+      p2 = c_div(c_sub<X>(c_mul<X>(a, p1), c_mul<X>((double)n, p0)), (double)(n + 1));
+    } else {
+      p2 = p_next(n, x, p1, p0);
+    }
     const double d2 = c_add<X>(d0, c_mul<X>(k2, p1));
     const double e2 = c_add<X>(e0, c_mul<X>(k2, d1));
     const double cxn = C.cx[n + 1], cyn = C.cy[n + 1];
@@ -119,6 +145,42 @@ __host__ __device__ inline void curve_eval_d(const CurveRef& C, double tau, doub
   g1[1] = c_mul<X>(2.0, g1[1]);
   g2[0] = c_mul<X>(4.0, g2[0]);
   g2[1] = c_mul<X>(4.0, g2[1]);
+}
+
+// G and dG/dtau only (the Newton steps never need G''); same operations as
+// curve_eval_d for the two outputs
+template <bool X>
+__host__ __device__ inline void curve_eval_d1(const CurveRef& C, double tau, double g[2], double g1[2]) {
+  const double x = c_sub<X>(c_mul<X>(2.0, tau), 1.0);
+  double p0 = 1.0, p1 = x, d0 = 0.0, d1 = 1.0;
+  g[0] = C.cx[0];
+  g[1] = C.cy[0];
+  g1[0] = g1[1] = 0.0;
+  if (C.D >= 1) {
+    g[0] = c_add<X>(g[0], c_mul<X>(C.cx[1], x));
+    g[1] = c_add<X>(g[1], c_mul<X>(C.cy[1], x));
+    g1[0] = c_add<X>(g1[0], c_mul<X>(C.cx[1], d1));
+    g1[1] = c_add<X>(g1[1], c_mul<X>(C.cy[1], d1));
+  }
+  for (int n = 1; n < C.D; ++n) {
+    const double k2 = (double)(2 * n + 1);
+    double p2;
+    if constexpr (X) {
+      const double a = c_mul<X>(k2, x);
+      p2 = c_div(c_sub<X>(c_mul<X>(a, p1), c_mul<X>((double)n, p0)), (double)(n + 1));
+    } else {
+      p2 = p_next(n, x, p1, p0);
+    }
+    const double d2 = c_add<X>(d0, c_mul<X>(k2, p1));
+    const double cxn = C.cx[n + 1], cyn = C.cy[n + 1];
+    g[0] = c_add<X>(g[0], c_mul<X>(cxn, p2));
+    g[1] = c_add<X>(g[1], c_mul<X>(cyn, p2));
+    g1[0] = c_add<X>(g1[0], c_mul<X>(cxn, d2));
+    g1[1] = c_add<X>(g1[1], c_mul<X>(cyn, d2));
+    p0 = p1; p1 = p2; d0 = d1; d1 = d2;
+  }
+  g1[0] = c_mul<X>(2.0, g1[0]);
+  g1[1] = c_mul<X>(2.0, g1[1]);
 }
 
 struct BlendGeom {
@@ -154,16 +216,25 @@ __host__ __device__ inline void blend_jac(const BlendGeom& B, const CurveRef& C,
   const double om0 = c_sub<X>(1.0, xi);
   const double om = om0 > 1e-13 ? om0 : 1e-13;
   const double lam = c_sub<X>(om0, eta);
-  double g[2], g1[2], g2[2];
-  curve_eval_d<X>(C, om, g, g1, g2);
+  double g[2], g1[2];
+  curve_eval_d1<X>(C, om, g, g1);
   const double bx = c_add<X>(c_add<X>(c_mul<X>(lam, B.PLx), c_mul<X>(xi, B.P0x)), c_mul<X>(eta, B.Ox));
   const double by = c_add<X>(c_add<X>(c_mul<X>(lam, B.PLy), c_mul<X>(xi, B.P0y)), c_mul<X>(eta, B.Oy));
   const double Dx = c_sub<X>(c_sub<X>(g[0], c_mul<X>(om, B.PLx)), c_mul<X>(xi, B.P0x));
   const double Dy = c_sub<X>(c_sub<X>(g[1], c_mul<X>(om, B.PLy)), c_mul<X>(xi, B.P0y));
-  const double r = c_div(lam, om);
+  double r, drx, dre;
+  if constexpr (X) {
+    r = c_div(lam, om);
+    drx = c_div(-eta, c_mul<X>(om, om));
+    dre = c_div(-1.0, om);
+  } else {
+    const double inv = 1.0 / om;
+    r = lam * inv;
+    dre = -inv;
+    drx = -eta * inv * inv;
+  }
   x = c_add<X>(bx, c_mul<X>(r, Dx));
   y = c_add<X>(by, c_mul<X>(r, Dy));
-  const double drx = c_div(-eta, c_mul<X>(om, om)), dre = c_div(-1.0, om);
   const double dDx = c_sub<X>(c_sub<X>(B.PLx, g1[0]), B.P0x), dDy = c_sub<X>(c_sub<X>(B.PLy, g1[1]), B.P0y);
   J[0] = c_add<X>(c_add<X>(c_sub<X>(B.P0x, B.PLx), c_mul<X>(drx, Dx)), c_mul<X>(r, dDx));
   J[1] = c_add<X>(c_sub<X>(B.Ox, B.PLx), c_mul<X>(dre, Dx));
@@ -180,8 +251,14 @@ __host__ __device__ inline void newton_step(const BlendGeom& B, const CurveRef& 
   blend_jac<X>(B, C, xi, eta, x, y, J);
   const double rx = c_sub<X>(tx, x), ry = c_sub<X>(ty, y);
   const double dj = c_sub<X>(c_mul<X>(J[0], J[3]), c_mul<X>(J[1], J[2]));
-  dxi = c_div(c_sub<X>(c_mul<X>(J[3], rx), c_mul<X>(J[1], ry)), dj);
-  deta = c_div(c_sub<X>(c_mul<X>(J[0], ry), c_mul<X>(J[2], rx)), dj);
+  if constexpr (X) {
+    dxi = c_div(c_sub<X>(c_mul<X>(J[3], rx), c_mul<X>(J[1], ry)), dj);
+    deta = c_div(c_sub<X>(c_mul<X>(J[0], ry), c_mul<X>(J[2], rx)), dj);
+  } else {
+    const double inv = 1.0 / dj;
+    dxi = (J[3] * rx - J[1] * ry) * inv;
+    deta = (J[0] * ry - J[2] * rx) * inv;
+  }
   xi = c_add<X>(xi, dxi);
   eta = c_add<X>(eta, deta);
 }
@@ -196,13 +273,15 @@ __host__ __device__ inline void blend_inverse(const BlendGeom& B, const CurveRef
   }
 }
 
-// Newton inverse to convergence (quadrature points: values, not predicates)
+// Newton inverse to convergence (quadrature points: values, not predicates).
+// Quadratic convergence: after a step of size delta the error is O(delta^2),
+// so stopping at delta < tol leaves ~tol^2.
 __host__ __device__ inline void blend_inverse_tol(const BlendGeom& B, const CurveRef& C, double tx, double ty,
-                                                  double& xi, double& eta) {
+                                                  double& xi, double& eta, double tol = 1e-15) {
   for (int it = 0; it < 40; ++it) {
     double dxi, deta;
     newton_step<false>(B, C, tx, ty, xi, eta, dxi, deta);
-    if (fabs(dxi) + fabs(deta) < 1e-15) break;
+    if (fabs(dxi) + fabs(deta) < tol) break;
   }
 }
 

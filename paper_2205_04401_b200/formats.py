@@ -1,8 +1,10 @@
 """Text formats of the reference specification.
 
 * Mesh file: header ``NV NE``; ``v x y bflag`` lines; then
-  ``e i j k kind [opp curve s_a s_b]`` lines (kind 0 = straight).  Written
-  with 17 significant digits so a write/read round trip is bit-exact.
+  ``e i j k kind [opp curve s_a s_b]`` lines (kind 0 = straight, otherwise a
+  curved element).  Written with 17 significant digits so
+  a write/read round trip is bit-exact.
+* Boundary-curve samples (curve.hpp:164-183): ``t x y dx dy`` rows.
 * Node CSV: ``x,y,u`` per target.
 * Sweep CSV (offload_sweep): ``Nf,TF,TN,TS,Ttot,c,sn``.
 * Quadrature-rule table (rules.hpp:87-103): ``kind N len`` then ``x y w``.
@@ -14,7 +16,9 @@ import io
 import numpy as np
 
 
-def write_mesh(path, vxy, tri, bflag=None):
+def write_mesh(path, vxy, tri, bflag=None, meta=None):
+    """meta: optional rows (kind, opp, curve, s_a, s_b) per element; kind 0 =
+    straight (annotate_boundary output)."""
     vxy = np.asarray(vxy, dtype=np.float64).reshape(-1, 2)
     tri = np.asarray(tri, dtype=np.int64).reshape(-1, 3)
     bflag = np.zeros(len(vxy), dtype=np.int64) if bflag is None else np.asarray(bflag, dtype=np.int64)
@@ -22,12 +26,18 @@ def write_mesh(path, vxy, tri, bflag=None):
         f.write(f"{len(vxy)} {len(tri)}\n")
         for (x, y), b in zip(vxy, bflag):
             f.write(f"v {x:.17g} {y:.17g} {int(b)}\n")
-        for i, j, k in tri:
-            f.write(f"e {i} {j} {k} 0\n")
+        for e, (i, j, k) in enumerate(tri):
+            if meta is not None and int(meta[e][0]) != 0:
+                kind, opp, cur, sa, sb = meta[e]
+                f.write(f"e {i} {j} {k} {int(kind)} {int(opp)} {int(cur)} {float(sa):.17g} {float(sb):.17g}\n")
+            else:
+                f.write(f"e {i} {j} {k} 0\n")
 
 
-def read_mesh(path):
-    """Returns (vxy, tri, bflag); raises ValueError naming the violated invariant."""
+def read_mesh(path, with_meta=False):
+    """Returns (vxy, tri, bflag), plus the per-element curved-side metadata
+    rows (kind, opp, curve, s_a, s_b) with with_meta=True; raises ValueError
+    naming the violated invariant."""
     with open(path) as f:
         head = f.readline().split()
         if len(head) != 2:
@@ -36,6 +46,7 @@ def read_mesh(path):
         vxy = np.zeros((nv, 2))
         bflag = np.zeros(nv, dtype=np.int64)
         tri = np.zeros((ne, 3), dtype=np.int32)
+        meta = np.zeros((ne, 5))
         for i in range(nv):
             t = f.readline().split()
             if len(t) < 4 or t[0] != "v":
@@ -46,12 +57,35 @@ def read_mesh(path):
             t = f.readline().split()
             if len(t) < 5 or t[0] != "e":
                 raise ValueError(f"mesh file: malformed element line {i}")
-            if int(t[4]) != 0:
-                raise ValueError("mesh file: curved elements are not supported (SURVEY.md §8(f3))")
             tri[i] = int(t[1]), int(t[2]), int(t[3])
+            kind = int(t[4])
+            if kind != 0:
+                if not with_meta:
+                    raise ValueError("mesh file: curved elements need read_mesh(..., with_meta=True)")
+                if len(t) < 9:
+                    raise ValueError(f"mesh file: curved element line {i} needs `opp curve s_a s_b`")
+                opp = int(t[5])
+                if opp < 0 or opp > 2:
+                    raise ValueError(f"mesh file: opposite-vertex index of element {i} not in 0..2")
+                meta[i] = kind, opp, int(t[6]), float(t[7]), float(t[8])
     if tri.size and (tri.min() < 0 or tri.max() >= nv):
         raise ValueError("mesh file: element vertex index out of range")
-    return vxy, tri, bflag
+    return (vxy, tri, bflag, meta) if with_meta else (vxy, tri, bflag)
+
+
+def read_curve_samples(path_or_buf):
+    """Hermite boundary-curve samples, one `t x y dx dy` row per line, `#`
+    comments (curve.hpp:164-183)."""
+    text = path_or_buf.read() if hasattr(path_or_buf, "read") else open(path_or_buf).read()
+    rows = []
+    for line in text.splitlines():
+        if not line.strip() or line.lstrip().startswith("#"):
+            continue
+        tok = line.split()
+        if len(tok) < 5:
+            raise ValueError("curve file: expected `t x y dx dy` per line")
+        rows.append([float(v) for v in tok[:5]])
+    return np.array(rows).reshape(-1, 5)
 
 
 def write_nodes_csv(path, txy, u):

@@ -170,3 +170,42 @@ def test_set_curves_usage_errors(disk):
         bad = vp.Curves(cv.curve_id, cv.deg, cv.cx, cv.cy, -cv.length)
         with pytest.raises(vp.VolpotError):
             ev.set_curves(bad)
+
+
+def test_ellipse_domain_on_gpu_matches_oracle_and_exact():
+    """Arc-length ellipse boundary (BoundaryCurve + annotate_boundary):
+    GPU vs oracle (lists, counts, u) and f = 1 against the closed form."""
+    from scipy.integrate import quad
+    a, b = 2.0, 1.0
+    pr = vp.load_config(2)
+    E = vp.BoundaryCurve.ellipse(a, b)
+    meta, vxy = vp.annotate_boundary(pr.vxy * np.array([a, b]), pr.tri, [E])
+    tri, cv = vp.curves_from_annotation(vxy, pr.tri, meta, [E])
+    r = vp.make_rules(50, eps=1e-12)
+    co = const_coeffs(len(tri), pr.p)
+    ev = vp.Evaluator(0)
+    ev.set_mesh(vxy, tri)
+    ev.set_curves(cv)
+    ev.set_rules(r)
+    ev.set_density(pr.p, co)
+    s_ = np.linspace(0, E.length, 3001)[:-1]
+    bpts = E.points(s_)[0] * (1 - np.linspace(0, 1e-3, s_.size))[:, None]
+    txy = np.concatenate([pr.txy * np.array([a, b]), bpts])
+    u, st = ev.evaluate(txy)
+    R = lambda th: a * b / np.sqrt((b * np.cos(th)) ** 2 + (a * np.sin(th)) ** 2)
+    C0 = sum(quad(lambda th: R(th) ** 2 / 2 * np.log(R(th)) - R(th) ** 2 / 4, k * np.pi / 4, (k + 1) * np.pi / 4,
+                  epsabs=1e-16, epsrel=1e-16)[0] for k in range(8)) / (2 * np.pi)
+    exact = C0 + (b * txy[:, 0] ** 2 + a * txy[:, 1] ** 2) / (2 * (a + b))
+    assert np.abs(u - exact).max() <= 5e-12
+    assert st["n_outside"] == 0
+    O = Oracle(vxy, tri, pr.p, co, r, curves=cv)
+    sub = np.concatenate([txy[:-3000][::211], bpts[::5]])
+    s_g, off_g, ids_g = ev.build_nearlist(sub)
+    s_o, off_o, ids_o = O.nearlist(sub)
+    assert np.array_equal(s_g, s_o) and np.array_equal(ids_g, ids_o)
+    u_g, st_g = ev.evaluate(sub)
+    u_o, _, st_o = O.evaluate(sub)
+    assert rel(u_g, u_o) <= REL_TOL
+    for k in ("n_leaves", "n_panels", "n_degenerate", "n_rho_le1"):
+        assert st_g[k] == st_o[k], k
+    ev.close()
