@@ -343,6 +343,9 @@ __global__ void k_far_reduce(int64_t T, int nsplit, const double* __restrict__ p
 // (k_far / k_fmm_eval with ZERO_CHECK=false), so it cancels, as the oracle's
 // skipped pair does.  The per-pair API (vp_near_pairs / vp_self_pairs) uses
 // exact_zero = true so its point sum matches SPEC.md:575 on its own.
+// ltab: a single-copy table (STRIDE 1) or this lane's copy of the replicated
+// one (tab + (lane & 7), STRIDE kLogCopies)
+template <int STRIDE = 1>
 __device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q, double tx,
                                                  double ty, const double* __restrict__ sx,
                                                  const double* __restrict__ sy,
@@ -353,7 +356,7 @@ __device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q,
     const int64_t k = e * len_q + i;
     const double dx = tx - sx[k], dy = ty - sy[k];
     const double r2 = fma(dx, dx, dy * dy);
-    const double lg = exact_zero ? fast_log_r2<1, true>(ltab, r2) : fast_log_r2<1, false>(ltab, r2);
+    const double lg = exact_zero ? fast_log_r2<STRIDE, true>(ltab, r2) : fast_log_r2<STRIDE, false>(ltab, r2);
     s = fma(sq[k], lg, s);
   }
   return warp_sum(s);
@@ -448,6 +451,11 @@ __device__ __forceinline__ void side_lengths0(const ElemRec& E, double l0[3]) {
   }
 }
 
+// Count pass (FILL = false): counts every pair's leaves and keeps the first
+// `cap` codes in scratch[p * cap ..]; pairs with more append themselves to
+// `over` and are walked again by the fill pass (FILL = true, over `plist`),
+// the others are copied by k_leaves_copy -- one full subdivision per pair
+// instead of two.
 template <bool FILL>
 __global__ void __launch_bounds__(128)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
@@ -455,17 +463,20 @@ __global__ void __launch_bounds__(128)
                   const ElemRec* __restrict__ el, const RulesDev* __restrict__ R,
                   int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
                   unsigned long long* __restrict__ leaves, unsigned long long* __restrict__ stats,
-                  int* __restrict__ err, CurvesDev CV) {
+                  int* __restrict__ err, CurvesDev CV, const int32_t* __restrict__ plist,
+                  unsigned long long* __restrict__ scratch, int cap, int32_t* __restrict__ over,
+                  unsigned* __restrict__ n_over) {
   __shared__ double skd[kMaxNearDepth + 2];
   for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
   const double ball_factor = R->near_model == 1 ? R->ball_factor : 0.0;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t pi_ = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = plist ? (pi_ < n_pairs ? plist[pi_] : INT64_MAX) : pi_;
   unsigned long long rle1 = 0;
   int maxd = 0;
-  if (p < n_pairs && curve_id_of(CV, pair_elem[p]) >= 0) {
+  if (pi_ < n_pairs && curve_id_of(CV, pair_elem[p]) >= 0) {
     if (!FILL) cnt[p] = 0;  // curved element: k_near_curved
-  } else if (p < n_pairs) {
+  } else if (pi_ < n_pairs) {
     const int32_t e = pair_elem[p];
     const double2 tp = txy[pair_tgt[p]];
     const ElemRec E = el[e];
@@ -485,6 +496,7 @@ __global__ void __launch_bounds__(128)
       bool le1;
       if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0)) {
         if (FILL) leaves[o++] = code;
+        else if (n < cap) scratch[p * cap + n] = code;
         ++n;
         rle1 += le1 ? 1ull : 0ull;
         maxd = max(maxd, d);
@@ -501,7 +513,10 @@ __global__ void __launch_bounds__(128)
       }
     }
     if (bad) atomicExch(err, 2);
-    if (!FILL) cnt[p] = bad ? 0 : n;
+    if (!FILL) {
+      cnt[p] = bad ? 0 : n;
+      if (!bad && n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)p;
+    }
   }
   if (!FILL) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -515,7 +530,17 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Per-element cache of w_i f(xi_{slot,i}) at the N_n-rule nodes of every
+// leaves of the pairs that fit the count pass's scratch -> CSR leaf array
+__global__ void k_leaves_copy(int64_t n_pairs, const int64_t* __restrict__ off, int cap,
+                              const unsigned long long* __restrict__ scratch, unsigned long long* __restrict__ leaves) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int64_t o = off[p], n = off[p + 1] - o;
+  if (n > cap) return;
+  for (int64_t i = 0; i < n; ++i) leaves[o + i] = scratch[p * cap + i];
+}
+
+// Per-element cache of G = w_i f(xi_{slot,i}) |J_T| 4^-d / (4 pi) at the N_n-rule nodes of every
 // sub-simplex of depth <= D (slot = (4^d - 1)/3 + path): a dense
 // coefficient-to-value contraction G[e][r] = sum_j Vt[j][r] c_e[j] with the
 // host-built Vt[j][r] = w_i K_j(xi_{slot,i}), r = slot * Ln + i.  Each thread
@@ -523,13 +548,13 @@ __global__ void __launch_bounds__(128)
 constexpr int kCacheNE = 8;
 __global__ void __launch_bounds__(256)
     k_near_cache(int64_t E, int M, int64_t R, const double* __restrict__ Vt, const double* __restrict__ coeffs,
-                 double* __restrict__ out) {
+                 const ElemRec* __restrict__ el, double* __restrict__ out) {
   __shared__ double sc[kCacheNE][kMaxModes];
   const int64_t e0 = (int64_t)blockIdx.x * kCacheNE;  // x: element chunks (up to 2^31 - 1)
   const int ne = (int)min((int64_t)kCacheNE, E - e0);
   for (int i = threadIdx.x; i < kCacheNE * M; i += blockDim.x) {
     const int k = i / M, j = i - k * M;
-    sc[k][j] = k < ne ? coeffs[(e0 + k) * M + j] : 0.0;
+    sc[k][j] = k < ne ? coeffs[(e0 + k) * M + j] * el[e0 + k].det : 0.0;  // |J_T| folded in
   }
   __syncthreads();
   const int64_t r = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
@@ -684,29 +709,178 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, MODE == 0 ? 4 : VP_NEAR_MINB)
       }
     }
     const double val = warp_sum(acc);
-    if constexpr (MODE == 0) {
-      const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, exact_zero);
-      if (lane == 0) {
-        part[p] = val;
-        part_s[p] = sub;
-      }
-    } else {
-      if (lane == 0) part[p] = val;
-    }
+    if (lane == 0) part[p] = val;
   }
 }
 
-// corr = a + b - s (evaluation) or val = a + b, sub = s (per-pair API)
+// K4b, cached leaves (depth <= cache_depth): one warp per pair.  Each lane
+// owns fixed rule nodes (lane + 32 k), so a node's (u, v) stays in
+// registers and the leaf loop is uniform across the warp; per leaf the warp
+// reads (broadcast) the physical vectors D0 = t - P_a, BA = P_b - P_a,
+// CA = P_c - P_a of the sub-simplex, formed from the slot's reference
+// vertices (a per-slot table, no path decoding).  A node then costs
+// t - y = D0 - u BA - v CA (4 FMA), r^2 (2), the table log (6 FP64 + I2F)
+// and one FMA with the cached G = w f |J_T| 4^-d / (4 pi) (k_near_cache).
+// The cache exceeds L2 on large meshes, so each leaf's G values are loaded
+// one leaf ahead.  The log table is replicated 8x in dynamic shared memory
+// as in K2 (conflict-free quarter-warp loads).  r^2 = 0 cannot occur: a
+// near element never contains t and the rule's nodes are interior.  The
+// element's point sum (the subtract of subtract-and-add) is k_point_sum.
+constexpr int NC_WARPS = 12;
+template <int K>  // ceil(len_n / 32) rule nodes per lane
+__global__ void __launch_bounds__(NC_WARPS * 32, 2)
+    k_near_c(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
+             const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
+             const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
+             const double* __restrict__ gcache, const double* __restrict__ slot_ref, int cache_depth,
+             double* __restrict__ part, unsigned c3ff) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
+  __shared__ double4 sD[NC_WARPS][32];
+  __shared__ double2 sC[NC_WARPS][32];
+  __shared__ int sslot[NC_WARPS][32];
+  const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
+  const int Ln = R->len_n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nu[K], nv[K];
+  bool nok[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int n = lane + 32 * k;
+    nok[k] = n < Ln;
+    nu[k] = nok[k] ? R->near_x[n] : 0.0;
+    nv[k] = nok[k] ? R->near_y[n] : 0.0;
+  }
+  __syncthreads();
+  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t p = (int64_t)blockIdx.x * NC_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * NC_WARPS) {
+    const int32_t t = pair_tgt[p], e = pair_elem[p];
+    const int64_t l0 = loff[p], nl = loff[p + 1] - l0;
+    const double2 tp = txy[t];
+    const double tx = tp.x, ty = tp.y;
+    const double* gce = gcache + (int64_t)e * nslot * Ln + lane;
+    double acc = 0.0;
+    for (int64_t lb = 0; lb < nl; lb += 32) {
+      const int nb = (int)min((int64_t)32, nl - lb);
+      __syncwarp();
+      unsigned long long code = 0;
+      int d = 0;
+      bool mine = false;
+      if (lane < nb) {
+        code = leaves[l0 + lb + lane];
+        d = (int)(code >> 58);
+        mine = d <= cache_depth;
+      }
+      const unsigned mm = __ballot_sync(0xffffffffu, mine);
+      const int nm = __popc(mm);
+      if (nm == 0) continue;
+      if (mine) {
+        const ElemRec& Er = el[e];
+        const int pos = __popc(mm & lt_mask);
+        const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+        const double* r = slot_ref + 6 * slot;  // a, b - a, c - a of the slot (L1-resident)
+        const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
+        const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
+        sD[wid][pos] = make_double4(tx - pax, ty - pay, fma(r[3], Er.e2x, r[2] * Er.e1x),
+                                    fma(r[3], Er.e2y, r[2] * Er.e1y));
+        sC[wid][pos] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
+        sslot[wid][pos] = slot * Ln;
+      }
+      __syncwarp();
+      double gn[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) gn[k] = nok[k] ? __ldg(gce + sslot[wid][0] + 32 * k) : 0.0;
+#pragma unroll 1
+      for (int li = 0; li < nm; ++li) {
+        double g[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) g[k] = gn[k];
+        if (li + 1 < nm) {
+          const int sn = sslot[wid][li + 1];
+#pragma unroll
+          for (int k = 0; k < K; ++k) gn[k] = nok[k] ? __ldg(gce + sn + 32 * k) : 0.0;
+        }
+        const double4 dd = sD[wid][li];
+        const double2 cc = sC[wid][li];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (k + 1 < K || nok[k]) {
+            const double dx = fma(-nu[k], dd.z, fma(-nv[k], cc.x, dd.x));
+            const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
+            acc = fma(g[k], far_log_r2<false>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
+          }
+        }
+      }
+    }
+    const double val = warp_sum(acc);
+    if (lane == 0) part[p] = val;
+  }
+}
+
+// Point sums of subtract-and-add for the per-pair API: part_s[p] =
+// sum_{i in T} q_i log r_{t,i}^2 (coincident pairs exactly 0);
+// warp per pair, lanes over T's sources.
+constexpr int PS_WARPS = 8;
+__global__ void __launch_bounds__(PS_WARPS * 32)
+    k_point_sum(int64_t n_pairs, const int32_t* __restrict__ pair_tgt, const int32_t* __restrict__ pair_elem,
+                const double2* __restrict__ txy, int len_q, const double* __restrict__ sx,
+                const double* __restrict__ sy, const double* __restrict__ sq, double* __restrict__ part_s,
+                bool exact_zero) {
+  __shared__ double2 sltab[kLogEntries];
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t p = (int64_t)blockIdx.x * PS_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * PS_WARPS) {
+    const double2 tp = txy[pair_tgt[p]];
+    const double sub = warp_point_sum(lane, pair_elem[p], len_q, tp.x, tp.y, sx, sy, sq, sltab, exact_zero);
+    if (lane == 0) part_s[p] = sub;
+  }
+}
+
+// corr = a + b; per-pair API: sub = s
 __global__ void k_near_combine(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
                                const double* __restrict__ s, double* __restrict__ corr, double* __restrict__ sub_out) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const double v = a[p] + b[p];
-  if (sub_out) {
-    corr[p] = v;
-    sub_out[p] = s[p];
-  } else {
-    corr[p] = v - s[p];
+  corr[p] = a[p] + b[p];
+  if (sub_out) sub_out[p] = s[p];
+}
+
+// The evaluation's subtract of subtract-and-add, per
+// target: psum[t] = sum over S(t) and N(t) of the elements' point sums
+// q_i log r^2.  Warp per target, lanes over the flattened (element, source)
+// items, so one reduction serves all of t's pairs.  Coincident pairs take the
+// far sum's own no-zero-check log and cancel with it.
+constexpr int PT_WARPS = 8;
+__global__ void __launch_bounds__(PT_WARPS * 32)
+    k_psum_tgt(int64_t T, const double2* __restrict__ txy, const int32_t* __restrict__ self,
+               const int64_t* __restrict__ off, const int32_t* __restrict__ ids, int len_q,
+               const double* __restrict__ sx, const double* __restrict__ sy, const double* __restrict__ sq,
+               double* __restrict__ psum) {
+  __shared__ double2 sltab[kLogEntries];
+  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t t = (int64_t)blockIdx.x * PT_WARPS + wid; t < T; t += (int64_t)gridDim.x * PT_WARPS) {
+    const double2 tp = txy[t];
+    const int32_t se = self[t];
+    const int64_t o0 = off[t], nn = off[t + 1] - o0;
+    const int first = se >= 0 ? 0 : 1;  // item block 0 = S(t), blocks 1.. = N(t)
+    const int64_t items = (nn + 1 - first) * (int64_t)len_q;
+    double s = 0.0;
+    int blk = first + lane / len_q, src = lane - (lane / len_q) * len_q;
+    for (int64_t j = lane; j < items; j += 32) {
+      const int32_t e = blk == 0 ? se : ids[o0 + blk - 1];
+      const int64_t k = (int64_t)e * len_q + src;
+      const double dx = tp.x - sx[k], dy = tp.y - sy[k];
+      s = fma(sq[k], fast_log_r2<1, false>(sltab, fma(dx, dx, dy * dy)), s);
+      src += 32;
+      while (src >= len_q) { src -= len_q; ++blk; }
+    }
+    s = warp_sum(s);
+    if (lane == 0) psum[t] = s;
   }
 }
 
@@ -928,9 +1102,11 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
     const double val = warp_sum(acc) * kInv2Pi;
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
+    // the evaluation subtracts every point sum of t at once (k_psum_tgt); the
+    // per-pair API returns this element's own
+    const double sub = sub_out ? warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, true) : 0.0;
     if (lane == 0) {
-      corr[it] = sub_out ? val : val - sub;
+      corr[it] = val;
       if (sub_out) sub_out[it] = sub;
       if (panels_out) panels_out[it] = npan_item;
       my_panels += (unsigned long long)npan_item;
@@ -1062,9 +1238,9 @@ __global__ void __launch_bounds__(CURV_WARPS * 32)
       }
     }
     const double val = warp_sum(acc);
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
+    const double sub = sub_out ? warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, true) : 0.0;
     if (lane == 0) {
-      corr[p] = sub_out ? val : val - sub;
+      corr[p] = val;
       if (sub_out) sub_out[p] = sub;
       if (lcnt) lcnt[p] = bad ? 0 : nleaf;
       if (bad) atomicExch(err, 2);
@@ -1211,9 +1387,11 @@ __global__ void __launch_bounds__(CURV_WARPS * 32)
         if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
     const double val = warp_sum(acc) * kInv2Pi;
-    const double sub = warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, sub_out != nullptr);
+    // the evaluation subtracts every point sum of t at once (k_psum_tgt); the
+    // per-pair API returns this element's own
+    const double sub = sub_out ? warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, true) : 0.0;
     if (lane == 0) {
-      corr[it] = sub_out ? val : val - sub;
+      corr[it] = val;
       if (sub_out) sub_out[it] = sub;
       if (panels_out) panels_out[it] = npan_item;
       my_panels += (unsigned long long)npan_item;
@@ -1345,12 +1523,13 @@ __global__ void __launch_bounds__(128)
   out[i] = density<P>(cc, xi, eta);
 }
 
-__global__ void k_assemble(int64_t T, const double* __restrict__ ufar, const int64_t* __restrict__ off,
-                           const double* __restrict__ corr, const double* __restrict__ corr_self,
-                           double* __restrict__ u) {
+// u = (u_far - psum) + sum of near values + self value
+__global__ void k_assemble(int64_t T, const double* __restrict__ ufar, const double* __restrict__ psum,
+                           const int64_t* __restrict__ off, const double* __restrict__ corr,
+                           const double* __restrict__ corr_self, double* __restrict__ u) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
-  double s = ufar[t];
+  double s = ufar[t] - psum[t];
   for (int64_t p = off[t]; p < off[t + 1]; ++p) s += corr[p];
   s += corr_self[t];
   u[t] = s;
@@ -1460,7 +1639,8 @@ struct vp_ctx {
   double ball_factor = 1.5;
   int cache_max_depth = 3, cache_depth = -1;
   int64_t cache_max_bytes = 12ll << 30;
-  DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps;
+  DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
+  int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
@@ -1684,15 +1864,41 @@ int build_elements(vp_ctx* c) {
     default: break;                     \
   }
 
+template <int K>
+void launch_near_c(vp_ctx* c, int blocks, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
+                   const double* gc) {
+  k_near_c<K><<<std::max(blocks, 1), NC_WARPS * 32, sizeof(LogTab), c->stream>>>(
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_loff.as<int64_t>(), c->d_leafcodes.as<unsigned long long>(),
+      c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, c->d_npa.as<double>(), 0x3ff00000u);
+}
+
+#define VP_DISPATCH_K(k, F, ...)     \
+  switch (k) {                       \
+    case 1: F<1>(__VA_ARGS__); break; \
+    case 2: F<2>(__VA_ARGS__); break; \
+    case 3: F<3>(__VA_ARGS__); break; \
+    case 4: F<4>(__VA_ARGS__); break; \
+    case 5: F<5>(__VA_ARGS__); break; \
+    case 6: F<6>(__VA_ARGS__); break; \
+    case 7: F<7>(__VA_ARGS__); break; \
+    default: F<8>(__VA_ARGS__); break; \
+  }
+
 template <int P>
 void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
                      double* corr, double* sub) {
   const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 32);
   const double* gc = c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr;
-  k_near_int<P, 0><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
-      c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-      c->d_rules.as<RulesDev>(), gc, c->cache_depth, c->d_npa.as<double>(), c->d_nps.as<double>(), sub != nullptr);
+  const int cblocks = (int)std::min<int64_t>(nblk(n, NC_WARPS), (int64_t)c->sm_count * 16);
+  if (sub)
+    k_point_sum<<<(unsigned)std::min<int64_t>(nblk(n, PS_WARPS), (int64_t)c->sm_count * 64), PS_WARPS * 32, 0,
+                  c->stream>>>(n, ptgt, pelem, txy, c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                               c->d_sq.as<double>(), c->d_nps.as<double>(), true);
+  if (c->cache_depth >= 0) {
+    VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_c, c, cblocks, n, ptgt, pelem, txy, gc);
+  } else {
+    cudaMemsetAsync(c->d_npa.p, 0, sizeof(double) * n, c->stream);
+  }
   k_near_int<P, 1><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
       c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
@@ -1717,9 +1923,16 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
                 double* corr, double* sub, int64_t* leaves_host) {
   CUDA_TRY(c, c->d_lcnt.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_loff.ensure(sizeof(int64_t) * (n + 1)));
+  // scratch for the first `cap` leaves of every pair, within a memory budget
+  const int cap = (int)std::min<int64_t>(64, (c->leaf_scratch_budget / 8) / std::max<int64_t>(n, 1));
+  CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
+  CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
+  CUDA_TRY(c, c->d_nover.ensure(sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, sizeof(unsigned), c->stream));
   k_near_leaves<false><<<nblk(n, 128), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), nullptr,
-      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c));
+      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
+      c->d_lscratch.as<unsigned long long>(), cap, c->d_lover.as<int32_t>(), c->d_nover.as<unsigned>());
   CUDA_TRY(c, cudaMemsetAsync(c->d_lcnt.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1, c->stream);
@@ -1727,14 +1940,20 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1,
                                 c->stream);
   int64_t nleaves = 0;
+  unsigned nover = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&nleaves, c->d_loff.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
                               c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&nover, c->d_nover.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   CUDA_TRY(c, c->d_leafcodes.ensure(sizeof(unsigned long long) * (nleaves + 1)));
-  k_near_leaves<true><<<nblk(n, 128), 128, 0, c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
-      c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>(),
-      curves_dev(c));
+  k_leaves_copy<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_loff.as<int64_t>(), cap,
+                                                     c->d_lscratch.as<unsigned long long>(),
+                                                     c->d_leafcodes.as<unsigned long long>());
+  if (nover > 0)
+    k_near_leaves<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
+        nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
+        c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>(),
+        curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0, nullptr, nullptr);
   if (int rc = build_near_cache(c)) return rc;
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
@@ -1746,7 +1965,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   }
   CUDA_TRY(c, cudaGetLastError());
   c->n_leaves_last = nleaves;
-  c->last_launches += 7;
+  c->last_launches += 8;
   if (leaves_host)
     CUDA_TRY(c, cudaMemcpyAsync(leaves_host, c->d_lcnt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
   return 0;
@@ -1801,25 +2020,34 @@ int build_near_cache(vp_ctx* c) {
   if (D < 0) return 0;
   const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3, R = nslot * Ln;
   if (c->cacheV_depth != D || c->cacheV_p != c->p) {
-    std::vector<double> Vt((size_t)M * R), kv(M);
+    std::vector<double> Vt((size_t)M * R), kv(M), sref(6 * nslot);
     const vp_rules& r = c->rules;
     for (int d = 0; d <= D; ++d) {
       const int64_t off = ((1ll << (2 * d)) - 1) / 3, n = 1ll << (2 * d);
       for (int64_t path = 0; path < n; ++path) {
         double v[6];
         host_decode_path((unsigned long long)path, d, v);
+        double* sr = &sref[6 * (off + path)];
+        sr[0] = v[0]; sr[1] = v[1];
+        sr[2] = v[2] - v[0]; sr[3] = v[3] - v[1];
+        sr[4] = v[4] - v[0]; sr[5] = v[5] - v[1];
         for (int i = 0; i < Ln; ++i) {
           const double u = r.near_x[i], w = r.near_y[i];
           const double xi = v[0] + (u * (v[2] - v[0]) + w * (v[4] - v[0]));
           const double eta = v[1] + (u * (v[3] - v[1]) + w * (v[5] - v[1]));
           koorn_eval(c->p, xi, eta, kv.data());
           const int64_t row = (off + path) * Ln + i;
-          for (int j = 0; j < M; ++j) Vt[(size_t)j * R + row] = r.near_w[i] * kv[j];
+          // leaf scale 4^-d / (4 pi) folded in; k_near_cache multiplies by det
+          const double sc = std::ldexp(1.0, -2 * d) * kInv4Pi;
+          for (int j = 0; j < M; ++j) Vt[(size_t)j * R + row] = (r.near_w[i] * kv[j]) * sc;
         }
       }
     }
     CUDA_TRY(c, c->d_cacheV.ensure(sizeof(double) * Vt.size()));
     CUDA_TRY(c, cudaMemcpyAsync(c->d_cacheV.p, Vt.data(), sizeof(double) * Vt.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+    CUDA_TRY(c, c->d_slotref.ensure(sizeof(double) * sref.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_slotref.p, sref.data(), sizeof(double) * sref.size(), cudaMemcpyHostToDevice,
                                 c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->cacheV_depth = D;
@@ -1829,7 +2057,7 @@ int build_near_cache(vp_ctx* c) {
   if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
   dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
   k_near_cache<<<grid, 256, 0, c->stream>>>(c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(),
-                                            c->d_gcache.as<double>());
+                                            c->d_el.as<ElemRec>(), c->d_gcache.as<double>());
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 1;
   return 0;
@@ -2119,10 +2347,16 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
                 nullptr, nullptr);
   c->last_launches += 1;
   CUDA_TRY(c, cudaEventRecord(ev[4], c->stream));
-  k_assemble<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_ufar.as<double>(), c->d_off.as<int64_t>(),
-                                                   c->d_corr.as<double>(), c->d_corr_self.as<double>(), u);
+  CUDA_TRY(c, c->d_psum.ensure(sizeof(double) * (T + 1)));
+  k_psum_tgt<<<(unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64), PT_WARPS * 32, 0,
+               c->stream>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
+                            c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
+                            c->d_psum.as<double>());
+  k_assemble<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_ufar.as<double>(), c->d_psum.as<double>(),
+                                                   c->d_off.as<int64_t>(), c->d_corr.as<double>(),
+                                                   c->d_corr_self.as<double>(), u);
   k_count_self<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_self.as<int32_t>(), c->d_stats.as<unsigned long long>());
-  c->last_launches += 2;
+  c->last_launches += 3;
   CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
   CUDA_TRY(c, cudaGetLastError());
   unsigned long long hs[8];
@@ -2203,7 +2437,15 @@ int vp_create(int device, vp_ctx** out) {
     vp_destroy(c);
     return 3;
   }
-  if (cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+  if (cudaFuncSetAttribute(k_near_c<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
