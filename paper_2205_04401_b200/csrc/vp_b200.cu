@@ -451,18 +451,32 @@ __device__ __forceinline__ void side_lengths0(const ElemRec& E, double l0[3]) {
   }
 }
 
-// Count pass (FILL = false): counts every pair's leaves and keeps the first
-// `cap` codes in scratch[p * cap ..]; pairs with more append themselves to
-// `over` and are walked again by the fill pass (FILL = true, over `plist`),
-// the others are copied by k_leaves_copy -- one full subdivision per pair
-// instead of two.
+// Leaves are kept in two CSR arrays: depth <= D (the cached levels, K4b
+// k_near_c) and depth > D (k_near_int).  Count pass (FILL = false): counts
+// every pair's leaves of both kinds (cnt = total, cntc, cntd), keeps the
+// first `cap` codes in scratch[p * cap ..] and lists the pairs that have
+// deep leaves (`deep`); pairs with more than `cap` leaves append themselves
+// to `over` and are walked again by the fill pass (FILL = true, over
+// `plist`), the others are distributed by k_leaves_copy -- one full
+// subdivision per pair instead of two.
+struct LeafOut {
+  int64_t* cntc;
+  int64_t* cntd;
+  const int64_t* offc;
+  const int64_t* offd;
+  unsigned long long* leafc;
+  unsigned long long* leafd;
+  int32_t* deep;
+  unsigned* n_deep;
+  int D;
+};
+
 template <bool FILL>
 __global__ void __launch_bounds__(128)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
                   const int32_t* __restrict__ pair_elem, const double2* __restrict__ txy,
                   const ElemRec* __restrict__ el, const RulesDev* __restrict__ R,
-                  int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
-                  unsigned long long* __restrict__ leaves, unsigned long long* __restrict__ stats,
+                  int64_t* __restrict__ cnt, LeafOut lo, unsigned long long* __restrict__ stats,
                   int* __restrict__ err, CurvesDev CV, const int32_t* __restrict__ plist,
                   unsigned long long* __restrict__ scratch, int cap, int32_t* __restrict__ over,
                   unsigned* __restrict__ n_over) {
@@ -475,7 +489,7 @@ __global__ void __launch_bounds__(128)
   unsigned long long rle1 = 0;
   int maxd = 0;
   if (pi_ < n_pairs && curve_id_of(CV, pair_elem[p]) >= 0) {
-    if (!FILL) cnt[p] = 0;  // curved element: k_near_curved
+    if (!FILL) cnt[p] = lo.cntc[p] = lo.cntd[p] = 0;  // curved element: k_near_curved
   } else if (pi_ < n_pairs) {
     const int32_t e = pair_elem[p];
     const double2 tp = txy[pair_tgt[p]];
@@ -485,7 +499,7 @@ __global__ void __launch_bounds__(128)
     unsigned long long stack[kStackCap];
     int sp = 0;
     stack[sp++] = 0ull;
-    int64_t n = 0, o = FILL ? off[p] : 0;
+    int64_t n = 0, nc = 0, oc = FILL ? lo.offc[p] : 0, od = FILL ? lo.offd[p] : 0;
     bool bad = false;
     while (sp > 0) {
       const unsigned long long code = stack[--sp];
@@ -495,9 +509,14 @@ __global__ void __launch_bounds__(128)
       decode_path(path, d, ax, ay, bx, by, cx, cy);
       bool le1;
       if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0)) {
-        if (FILL) leaves[o++] = code;
-        else if (n < cap) scratch[p * cap + n] = code;
+        if (FILL) {
+          if (d <= lo.D) lo.leafc[oc++] = code;
+          else lo.leafd[od++] = code;
+        } else if (n < cap) {
+          scratch[p * cap + n] = code;
+        }
         ++n;
+        nc += d <= lo.D ? 1 : 0;
         rle1 += le1 ? 1ull : 0ull;
         maxd = max(maxd, d);
       } else {
@@ -514,8 +533,12 @@ __global__ void __launch_bounds__(128)
     }
     if (bad) atomicExch(err, 2);
     if (!FILL) {
-      cnt[p] = bad ? 0 : n;
-      if (!bad && n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)p;
+      if (bad) n = nc = 0;
+      cnt[p] = n;
+      lo.cntc[p] = nc;
+      lo.cntd[p] = n - nc;
+      if (n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)p;
+      if (n > nc) lo.deep[atomicAdd(lo.n_deep, 1u)] = (int32_t)p;
     }
   }
   if (!FILL) {
@@ -530,14 +553,19 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// leaves of the pairs that fit the count pass's scratch -> CSR leaf array
-__global__ void k_leaves_copy(int64_t n_pairs, const int64_t* __restrict__ off, int cap,
-                              const unsigned long long* __restrict__ scratch, unsigned long long* __restrict__ leaves) {
+// leaves of the pairs that fit the count pass's scratch -> the two CSR arrays
+__global__ void k_leaves_copy(int64_t n_pairs, const int64_t* __restrict__ cnt, int cap,
+                              const unsigned long long* __restrict__ scratch, LeafOut lo) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pairs) return;
-  const int64_t o = off[p], n = off[p + 1] - o;
+  const int64_t n = cnt[p];
   if (n > cap) return;
-  for (int64_t i = 0; i < n; ++i) leaves[o + i] = scratch[p * cap + i];
+  int64_t oc = lo.offc[p], od = lo.offd[p];
+  for (int64_t i = 0; i < n; ++i) {
+    const unsigned long long code = scratch[p * cap + i];
+    if ((int)(code >> 58) <= lo.D) lo.leafc[oc++] = code;
+    else lo.leafd[od++] = code;
+  }
 }
 
 // Per-element cache of G = w_i f(xi_{slot,i}) |J_T| 4^-d / (4 pi) at the N_n-rule nodes of every
@@ -612,7 +640,8 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, MODE == 0 ? 4 : VP_NEAR_MINB)
                const unsigned long long* __restrict__ leaves, const double* __restrict__ sx,
                const double* __restrict__ sy, const double* __restrict__ sq,
                const RulesDev* __restrict__ R, const double* __restrict__ gcache, int cache_depth,
-               double* __restrict__ part, double* __restrict__ part_s, bool exact_zero) {
+               double* __restrict__ part, double* __restrict__ part_s, bool exact_zero,
+               const int32_t* __restrict__ plist) {
   constexpr int M = (P + 1) * (P + 2) / 2;
   __shared__ double scc[MODE == 1 ? NEAR_WARPS : 1][M];
   __shared__ double2 sga[NEAR_WARPS][32], sgb[NEAR_WARPS][32], sgc[NEAR_WARPS][32];
@@ -631,7 +660,9 @@ __global__ void __launch_bounds__(NEAR_WARPS * 32, MODE == 0 ? 4 : VP_NEAR_MINB)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
-  for (int64_t p = (int64_t)blockIdx.x * NEAR_WARPS + wid; p < n_pairs; p += (int64_t)gridDim.x * NEAR_WARPS) {
+  for (int64_t pi_ = (int64_t)blockIdx.x * NEAR_WARPS + wid; pi_ < n_pairs;
+       pi_ += (int64_t)gridDim.x * NEAR_WARPS) {
+    const int64_t p = plist ? plist[pi_] : pi_;
     const int32_t t = pair_tgt[p], e = pair_elem[p];
     const double2 tp = txy[t];
     const double tx = tp.x, ty = tp.y;
@@ -887,6 +918,8 @@ __global__ void __launch_bounds__(PT_WARPS * 32)
 // ---------------------------------------------------------------------------
 // K5: self_eval in radius-arc-length coordinates.
 constexpr int SELF_WARPS = 4;
+// dyadic panels per side: N, M <= log2(L / dmin) + 1 <= 45 since dmin >= h > 1e-13 L
+constexpr int kMaxSelfPanels = 128;
 
 struct SelfGeom {
   double Ax, Ay, ABx, ABy, L, h, st;
@@ -960,8 +993,10 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
            int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV) {
   constexpr int M = (P + 1) * (P + 2) / 2;
   constexpr int NP = P + 1, NP2 = NP * NP;
+  constexpr int SNPT = NP2 <= 32 ? 1 : (NP2 <= 64 ? 2 : 3);
   __shared__ double scc[SELF_WARPS][M];
   __shared__ double sV[SELF_WARPS][NP2], sW[SELF_WARPS][NP2], sE[SELF_WARPS][2 * NP];
+  __shared__ double sB[SELF_WARPS][kMaxSelfPanels + 1];
   __shared__ double sPL[NP2], sgx[NP], sbt[NP], sct[NP], sla[NP], slb[NP];
   __shared__ double sglx[kMaxGL], sglw[kMaxGL];
   __shared__ double2 sltab[kLogEntries];
@@ -1026,16 +1061,21 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
       const double BRx = (k == 0 ? 1.0 : 0.0) - Arx, BRy = (k == 1 ? 1.0 : 0.0) - Ary;
       const double avx = Arx - txi, avy = Ary - teta;  // A - v in reference coordinates
-      // (1) f on the (p+1)^2 Gauss-Legendre grid (r_a, sigma_b), two points per call
-      for (int i = 2 * lane; i < NP2; i += 64) {
-        const int i2 = i + 1 < NP2 ? i + 1 : i;
-        const int a1 = i / NP, b1 = i - a1 * NP, a2 = i2 / NP, b2 = i2 - a2 * NP;
-        const double xs[2] = {fma(sgx[a1], fma(sgx[b1], BRx, avx), txi), fma(sgx[a2], fma(sgx[b2], BRx, avx), txi)};
-        const double ys[2] = {fma(sgx[a1], fma(sgx[b1], BRy, avy), teta), fma(sgx[a2], fma(sgx[b2], BRy, avy), teta)};
-        double f[2];
-        density_n<P, 2>(ShCoef(cc), xs, ys, f);
-        V[i] = f[0];
-        if (i + 1 < NP2) V[i + 1] = f[1];
+      // (1) f on the (p+1)^2 Gauss-Legendre grid (r_a, sigma_b), SNPT points per
+      // lane and call (one round of the warp for p <= 8)
+      for (int i = SNPT * lane; i < NP2; i += 32 * SNPT) {
+        double xs[SNPT], ys[SNPT], f[SNPT];
+#pragma unroll
+        for (int q = 0; q < SNPT; ++q) {
+          const int iq = min(i + q, NP2 - 1);
+          const int a = iq / NP, b = iq - a * NP;
+          xs[q] = fma(sgx[a], fma(sgx[b], BRx, avx), txi);
+          ys[q] = fma(sgx[a], fma(sgx[b], BRy, avy), teta);
+        }
+        density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
+#pragma unroll
+        for (int q = 0; q < SNPT; ++q)
+          if (i + q < NP2) V[i + q] = f[q];
       }
       __syncwarp();
       // (2) Legendre coefficients in r: W[n][b] = sum_a PL[n][a] V[a][b]
@@ -1066,12 +1106,17 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         sE[wid][o] = sum;
       }
       __syncwarp();
-      // (5) arc-length nodes: dyadic panels x Gauss-Legendre
-      const int nodes = G.npan * NL;
+      // (5) arc-length nodes: dyadic panels x Gauss-Legendre;
+      // the panel boundaries once per side in shared memory
+      const int npan = min(G.npan, kMaxSelfPanels);
+      for (int i = lane; i <= npan; i += 32) sB[wid][i] = self_bnd(G, i);
+      __syncwarp();
+      const int nodes = npan * NL;
       const double invL = 1.0 / G.L;
-      for (int j = lane; j < nodes; j += 32) {
-        const int pi = j / NL, gq = j - pi * NL;
-        const double s0 = self_bnd(G, pi), s1 = self_bnd(G, pi + 1);
+      int pi = lane / NL, gq = lane - pi * NL;
+      for (int j = lane; j < nodes; j += 32, gq += 32) {
+        while (gq >= NL) { gq -= NL; ++pi; }
+        const double s0 = sB[wid][pi], s1 = sB[wid][pi + 1];
         if (!(s1 > s0)) continue;
         const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
         const double s = fma(half, sglx[gq], mid);
@@ -1097,9 +1142,11 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         }
         acc = fma(ws * G.h, fma(lr0, ib, ic), acc);
       }
+      for (int i = 0; i < npan; i += 32) {
+        const bool nonempty = i + lane < npan && sB[wid][i + lane + 1] > sB[wid][i + lane];
+        npan_item += __popc(__ballot_sync(0xffffffffu, nonempty));
+      }
       __syncwarp();
-      for (int pi = 0; pi < G.npan; ++pi)
-        if (self_bnd(G, pi + 1) > self_bnd(G, pi)) ++npan_item;
     }
     const double val = warp_sum(acc) * kInv2Pi;
     // the evaluation subtracts every point sum of t at once (k_psum_tgt); the
@@ -1640,6 +1687,7 @@ struct vp_ctx {
   int cache_max_depth = 3, cache_depth = -1;
   int64_t cache_max_bytes = 12ll << 30;
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
+  DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
@@ -1868,7 +1916,7 @@ template <int K>
 void launch_near_c(vp_ctx* c, int blocks, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
                    const double* gc) {
   k_near_c<K><<<std::max(blocks, 1), NC_WARPS * 32, sizeof(LogTab), c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_loff.as<int64_t>(), c->d_leafcodes.as<unsigned long long>(),
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
       c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, c->d_npa.as<double>(), 0x3ff00000u);
 }
 
@@ -1886,8 +1934,8 @@ void launch_near_c(vp_ctx* c, int blocks, int64_t n, const int32_t* ptgt, const 
 
 template <int P>
 void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
-                     double* corr, double* sub) {
-  const int blocks = (int)std::min<int64_t>(nblk(n, NEAR_WARPS), (int64_t)c->sm_count * 32);
+                     double* corr, double* sub, int64_t ndeep) {
+  const int blocks = (int)std::min<int64_t>(nblk(ndeep, NEAR_WARPS), (int64_t)c->sm_count * 32);
   const double* gc = c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr;
   const int cblocks = (int)std::min<int64_t>(nblk(n, NC_WARPS), (int64_t)c->sm_count * 16);
   if (sub)
@@ -1899,10 +1947,14 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
   } else {
     cudaMemsetAsync(c->d_npa.p, 0, sizeof(double) * n, c->stream);
   }
-  k_near_int<P, 1><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loff.as<int64_t>(),
-      c->d_leafcodes.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-      c->d_rules.as<RulesDev>(), gc, c->cache_depth, c->d_npb.as<double>(), nullptr, sub != nullptr);
+  // deep leaves (depth > cache depth) of the listed pairs; the others add 0
+  cudaMemsetAsync(c->d_npb.p, 0, sizeof(double) * n, c->stream);
+  if (ndeep > 0)
+    k_near_int<P, 1><<<std::max(blocks, 1), NEAR_WARPS * 32, 0, c->stream>>>(
+        ndeep, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_loffd.as<int64_t>(),
+        c->d_leafd.as<unsigned long long>(), c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
+        c->d_rules.as<RulesDev>(), nullptr, -1, c->d_npb.as<double>(), nullptr, sub != nullptr,
+        c->d_ldeep.as<int32_t>());
   k_near_combine<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_npa.as<double>(), c->d_npb.as<double>(),
                                                      c->d_nps.as<double>(), corr, sub);
 }
@@ -1918,54 +1970,71 @@ void launch_near_curved(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t
 }
 
 int build_near_cache(vp_ctx* c);
+void decide_cache_depth(vp_ctx* c);
 
 int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
                 double* corr, double* sub, int64_t* leaves_host) {
+  decide_cache_depth(c);
   CUDA_TRY(c, c->d_lcnt.ensure(sizeof(int64_t) * (n + 1)));
-  CUDA_TRY(c, c->d_loff.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_lcntc.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_lcntd.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_loffc.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_loffd.ensure(sizeof(int64_t) * (n + 1)));
+  CUDA_TRY(c, c->d_ldeep.ensure(sizeof(int32_t) * (n + 1)));
   // scratch for the first `cap` leaves of every pair, within a memory budget
   const int cap = (int)std::min<int64_t>(64, (c->leaf_scratch_budget / 8) / std::max<int64_t>(n, 1));
   CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
-  CUDA_TRY(c, c->d_nover.ensure(sizeof(unsigned)));
-  CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, sizeof(unsigned), c->stream));
+  CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, 2 * sizeof(unsigned), c->stream));
+  LeafOut lo{c->d_lcntc.as<int64_t>(), c->d_lcntd.as<int64_t>(), c->d_loffc.as<int64_t>(), c->d_loffd.as<int64_t>(),
+             nullptr, nullptr, c->d_ldeep.as<int32_t>(), c->d_nover.as<unsigned>() + 1, c->cache_depth};
   k_near_leaves<false><<<nblk(n, 128), 128, 0, c->stream>>>(
-      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), nullptr,
-      nullptr, c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
+      n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), lo,
+      c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
       c->d_lscratch.as<unsigned long long>(), cap, c->d_lover.as<int32_t>(), c->d_nover.as<unsigned>());
-  CUDA_TRY(c, cudaMemsetAsync(c->d_lcnt.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_lcntc.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_lcntd.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1, c->stream);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_lcntc.as<int64_t>(), c->d_loffc.as<int64_t>(), n + 1, c->stream);
   CUDA_TRY(c, c->d_tmp.ensure(tmpb));
-  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_lcnt.as<int64_t>(), c->d_loff.as<int64_t>(), n + 1,
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_lcntc.as<int64_t>(), c->d_loffc.as<int64_t>(), n + 1,
                                 c->stream);
-  int64_t nleaves = 0;
-  unsigned nover = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&nleaves, c->d_loff.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+  cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_lcntd.as<int64_t>(), c->d_loffd.as<int64_t>(), n + 1,
+                                c->stream);
+  int64_t tot[2] = {0, 0};
+  unsigned nov[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(&tot[0], c->d_loffc.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
                               c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(&nover, c->d_nover.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&tot[1], c->d_loffd.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(nov, c->d_nover.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  CUDA_TRY(c, c->d_leafcodes.ensure(sizeof(unsigned long long) * (nleaves + 1)));
-  k_leaves_copy<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_loff.as<int64_t>(), cap,
-                                                     c->d_lscratch.as<unsigned long long>(),
-                                                     c->d_leafcodes.as<unsigned long long>());
+  const int64_t nleaves = tot[0] + tot[1];
+  const unsigned nover = nov[0], ndeep = nov[1];
+  CUDA_TRY(c, c->d_leafc.ensure(sizeof(unsigned long long) * (tot[0] + 1)));
+  CUDA_TRY(c, c->d_leafd.ensure(sizeof(unsigned long long) * (tot[1] + 1)));
+  lo.leafc = c->d_leafc.as<unsigned long long>();
+  lo.leafd = c->d_leafd.as<unsigned long long>();
+  k_leaves_copy<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_lcnt.as<int64_t>(), cap,
+                                                     c->d_lscratch.as<unsigned long long>(), lo);
   if (nover > 0)
     k_near_leaves<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
-        nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, c->d_loff.as<int64_t>(),
-        c->d_leafcodes.as<unsigned long long>(), c->d_stats.as<unsigned long long>(), c->d_err.as<int>(),
-        curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0, nullptr, nullptr);
+        nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, lo,
+        c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0,
+        nullptr, nullptr);
   if (int rc = build_near_cache(c)) return rc;
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
-  VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub);
+  VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub, (int64_t)ndeep);
   if (has_curves(c)) {
     VP_DISPATCH_P(c->p, launch_near_curved, c, n, ptgt, pelem, txy, corr, sub);
     c->last_launches += 1;
   }
   CUDA_TRY(c, cudaGetLastError());
   c->n_leaves_last = nleaves;
-  c->last_launches += 8;
+  c->last_launches += 9;
   if (leaves_host)
     CUDA_TRY(c, cudaMemcpyAsync(leaves_host, c->d_lcnt.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
   return 0;
@@ -2008,15 +2077,20 @@ static void host_decode_path(unsigned long long path, int d, double v[6]) {
 // Build (per evaluation) the per-element near-leaf cache: choose the depth
 // D <= cache_max_depth whose cache fits cache_max_bytes, build Vt on the host
 // once per (p, rules, D), then contract on the device.
-int build_near_cache(vp_ctx* c) {
-  const int Ln = c->rules.len_n, M = c->M;
+// deepest cached level whose per-element cache fits the byte budget (-1: none)
+void decide_cache_depth(vp_ctx* c) {
   int D = std::min(c->cache_max_depth, 6);
   while (D >= 0) {
     const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3;
-    if ((double)c->n_tri * nslot * Ln * 8.0 <= (double)c->cache_max_bytes) break;
+    if ((double)c->n_tri * nslot * c->rules.len_n * 8.0 <= (double)c->cache_max_bytes) break;
     --D;
   }
   c->cache_depth = D;
+}
+
+int build_near_cache(vp_ctx* c) {
+  const int Ln = c->rules.len_n, M = c->M;
+  const int D = c->cache_depth;
   if (D < 0) return 0;
   const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3, R = nslot * Ln;
   if (c->cacheV_depth != D || c->cacheV_p != c->p) {
