@@ -337,6 +337,15 @@ def main():
 
     if rank == 0:
         s0 = stats[-1]
+        list_ms = float(np.mean([s["t_list_ms"] for s in stats]))
+        list_bytes = 16 * T + 4 * T + 8 * (T + 1) + 4 * s0["n_near_pairs"] + 112 * pr.n_tri
+        try:
+            with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+                mp = json.load(f)
+            hbm_peak = next((float(v) for k, v in mp.items() if "hbm" in k.lower() and isinstance(v, (int, float))),
+                            None)
+        except (OSError, ValueError):
+            hbm_peak = None
         out = {
             "metric": "potential targets/sec (fp64)", "value": value, "unit": "targets/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -350,6 +359,12 @@ def main():
                        "l2": "flushed (256 MB write) between timed steps",
                        "parallelism": f"weak x{world} (targets sharded, mesh+density replicated)"},
             "near_pair_integrals_per_s": world * n_pairs / (pair_ms * 1e-3),
+            # K3 list build against HBM (SURVEY.md §8(d) bytes: targets 16T, S 4T, offsets
+            # 8(T+1), ids 4 P_near, element models 112 E); at config 2 it is launch/latency
+            # bound (two tiny passes + a scan), so this is reported, not a roofline claim
+            "list_build": {"ms": list_ms, "bytes": list_bytes,
+                           "GBps": list_bytes / (list_ms * 1e-3) / 1e9,
+                           "hbm_peak_GBps": hbm_peak},
             "split_ms": {"lib_device_total": float(np.mean([s["t_total_ms"] for s in stats])),
                          "list": float(np.mean([s["t_list_ms"] for s in stats])),
                          "sources": float(np.mean([s["t_sources_ms"] for s in stats])),
