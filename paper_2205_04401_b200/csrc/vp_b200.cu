@@ -395,10 +395,11 @@ __device__ __forceinline__ void decode_path(unsigned long long path, int d, doub
 // near_rec): rho_d = rho0n 4^{-d/N_n}; rho_d <= 1 accepts.
 constexpr int kBallMaxDepth = 20;  // ball model: accept at this depth (oracle: same)
 
+// g = (rd + 1/rd)/2 depends only on the depth: cached per thread in (gd, gv).
 __device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double ty, double rd,
                                             double ax, double ay, double bx, double by, double cx,
                                             double cy, bool& rle1, int d, double ball_factor,
-                                            const double l0[3]) {
+                                            const double l0[3], int& gd, double& gv) {
   rle1 = false;
   if (ball_factor > 0.0) {
     if (d >= kBallMaxDepth) return true;
@@ -415,7 +416,11 @@ __device__ __forceinline__ bool near_accept(const ElemRec& E, double tx, double 
     rle1 = true;
     return true;
   }
-  const double g = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+  if (d != gd) {
+    gd = d;
+    gv = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+  }
+  const double g = gv;
   const double vxs[3] = {ax, bx, cx}, vys[3] = {ay, by, cy};
   double dist[3];
 #pragma unroll
@@ -496,6 +501,8 @@ __global__ void __launch_bounds__(128)
     const ElemRec E = el[e];
     double l0[3];
     side_lengths0(E, l0);
+    int gd = -1;
+    double gv = 0.0;
     unsigned long long stack[kStackCap];
     int sp = 0;
     stack[sp++] = 0ull;
@@ -508,7 +515,8 @@ __global__ void __launch_bounds__(128)
       double ax, ay, bx, by, cx, cy;
       decode_path(path, d, ax, ay, bx, by, cx, cy);
       bool le1;
-      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0)) {
+      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd,
+                      gv)) {
         if (FILL) {
           if (d <= lo.D) lo.leafc[oc++] = code;
           else lo.leafd[od++] = code;
