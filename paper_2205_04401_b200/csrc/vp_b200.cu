@@ -828,18 +828,25 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
         sslot[wid][pos] = slot * Ln;
       }
       __syncwarp();
-      double gn[K];
+      // cache rows two leaves ahead (the cache exceeds L2 on large meshes)
+      double gn[K], gm[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) gn[k] = nok[k] ? __ldg(gce + sslot[wid][0] + 32 * k) : 0.0;
+      for (int k = 0; k < K; ++k) {
+        gn[k] = nok[k] ? __ldg(gce + sslot[wid][0] + 32 * k) : 0.0;
+        gm[k] = nok[k] && nm > 1 ? __ldg(gce + sslot[wid][1] + 32 * k) : 0.0;
+      }
 #pragma unroll 1
       for (int li = 0; li < nm; ++li) {
         double g[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) g[k] = gn[k];
-        if (li + 1 < nm) {
-          const int sn = sslot[wid][li + 1];
+        for (int k = 0; k < K; ++k) {
+          g[k] = gn[k];
+          gn[k] = gm[k];
+        }
+        if (li + 2 < nm) {
+          const int sn = sslot[wid][li + 2];
 #pragma unroll
-          for (int k = 0; k < K; ++k) gn[k] = nok[k] ? __ldg(gce + sn + 32 * k) : 0.0;
+          for (int k = 0; k < K; ++k) gm[k] = nok[k] ? __ldg(gce + sn + 32 * k) : 0.0;
         }
         const double4 dd = sD[wid][li];
         const double2 cc = sC[wid][li];
