@@ -324,7 +324,7 @@ def main():
         alt = {"far_method": other, "value": world * T * args.steps / (a_ms * 1e-3),
                "ms_per_step": a_ms / args.steps,
                "far_ms": float(np.mean([s["t_far_ms"] for s in a_st])),
-               "fmm_levels": a_st[-1]["fmm_levels"], "fmm_order": 36,
+               "fmm_levels": a_st[-1]["fmm_levels"], "fmm_order": 31,
                "max_rel_diff_u_vs_headline": diff}
         ev.set_far_method(args.far)
 

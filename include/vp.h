@@ -144,7 +144,7 @@ int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
 
 /* Far-field method: 0 = direct O(T S) sum (fmm_eval --direct, SPEC.md:618;
  * the default), 1 = 2-D Laplace FMM (fmm_eval; SURVEY.md
- * §8(f1)) with expansion order `order` (0 -> 36) and about `leaf_size`
+ * §8(f1)) with expansion order `order` (0 -> 31, 32 coefficients = one per lane) and about `leaf_size`
  * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity. */
 int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 

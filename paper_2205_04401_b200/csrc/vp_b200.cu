@@ -1692,7 +1692,7 @@ struct vp_ctx {
   // mesh bounding box (root of the FMM tree)
   double bx0 = 0, by0 = 0, bx1 = 0, by1 = 0;
   // far-field method: 0 direct (K2), 1 FMM
-  int far_method = 0, fmm_p = 36, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
+  int far_method = 0, fmm_p = 31, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
   int64_t fmm_outside = 0;
   DevBuf d_selftab;
   int selftab_p = -1;
@@ -2331,8 +2331,12 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   for (int l = 2; l <= L; ++l) {
     const int64_t nb = 1ll << (2 * l);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
-    k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+    if (P1 == 32)
+      k_fmm_m2l32<<<blocks, kFmmThreads, 0, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
                                                           c->f_lp.as<double2>());
+    else
+      k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+                                                            c->f_lp.as<double2>());
   }
   // L2P + P2P
   CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
@@ -2600,10 +2604,10 @@ int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
   if (!c) return 1;
   if (method != 0 && method != 1) return set_err(c, 1, "set_far_method: method must be 0 (direct) or 1 (fmm)");
   if (order != 0 && (order < 4 || order > kFmmMaxP))
-    return set_err(c, 1, "set_far_method: FMM order must be in [4, 62] (0 = default 36)");
+    return set_err(c, 1, "set_far_method: FMM order must be in [4, 62] (0 = default 31)");
   if (leaf_size < 0) return set_err(c, 1, "set_far_method: leaf size must be >= 0 (0 = default 40)");
   c->far_method = method;
-  c->fmm_p = order ? order : 36;
+  c->fmm_p = order ? order : 31;  // p + 1 = 32 coefficients: one per lane
   c->fmm_leaf = leaf_size ? leaf_size : 40;
   return 0;
 }

@@ -343,6 +343,87 @@ __global__ void __launch_bounds__(kFmmThreads)
   }
 }
 
+// The same downward pass specialised to p = 31 (32 coefficients, one per
+// lane): lane l keeps its column binA[1..31][l] of the M2L binomial matrix in
+// registers, so each source box costs 31 broadcast loads of e_k and 62 DFMA
+// per lane instead of two shared loads per pair of DFMA.
+__global__ void __launch_bounds__(kFmmThreads)
+    k_fmm_m2l32(FmmGeom g, int l, const double* __restrict__ tab, const double2* __restrict__ mp,
+                double2* __restrict__ lp) {
+  constexpr int P1 = 32;
+  __shared__ double binB[P1 * P1];
+  __shared__ double2 dpow[4 * P1];
+  __shared__ double2 ebuf[kFmmThreads / 32][P1];
+  FmmTabLayout TL(P1 - 1);
+  for (int i = threadIdx.x; i < P1 * P1; i += blockDim.x) binB[i] = tab[TL.binB + i];
+  for (int i = threadIdx.x; i < 4 * P1; i += blockDim.x)
+    dpow[i] = make_double2(tab[TL.dpow + 2 * i], tab[TL.dpow + 2 * i + 1]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double bc[P1];
+#pragma unroll
+  for (int k = 1; k < P1; ++k) bc[k] = tab[TL.binA + k * P1 + lane];
+  __syncthreads();
+  double2* e = ebuf[wid];
+  const double inv_l = lane > 0 ? 1.0 / lane : 0.0;
+  const double scl = ldexp(1.0, -lane);
+  const int n = 1 << l;
+  const int64_t nbox = (int64_t)n * n;
+  const double h = g.h0 / n;
+  const double logh = log(h);
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbox;
+       b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int ix = (int)(b % n), iy = (int)(b / n);
+    double2 acc = make_double2(0.0, 0.0);
+    if (l >= 3) {  // L2L from the parent (levels 0-2 carry no local expansion)
+      const int px = ix >> 1, py = iy >> 1, c = (ix & 1) | ((iy & 1) << 1);
+      const double2* par = lp + (lvl_off(l - 1) + (int64_t)py * (n >> 1) + px) * P1;
+      const double2* dp = dpow + c * P1;
+      __syncwarp();
+      e[lane] = par[lane];
+      __syncwarp();
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = lane; k < P1; ++k) {
+        const double bb = binB[k * P1 + lane];
+        s = cfma(e[k], make_double2(bb * dp[k - lane].x, bb * dp[k - lane].y), s);
+      }
+      acc = make_double2(s.x * scl, s.y * scl);
+    }
+    // interaction list: children of the parent's neighbours not adjacent to B
+    const int px = ix >> 1, py = iy >> 1;
+    for (int cy = 2 * py - 2; cy <= 2 * py + 3; ++cy) {
+      if (cy < 0 || cy >= n) continue;
+      for (int cx = 2 * px - 2; cx <= 2 * px + 3; ++cx) {
+        if (cx < 0 || cx >= n) continue;
+        const int dxi = cx - ix, dyi = cy - iy;
+        if (dxi >= -1 && dxi <= 1 && dyi >= -1 && dyi <= 1) continue;
+        const double2* src = mp + (lvl_off(l) + (int64_t)cy * n + cx) * P1;
+        const double2 a = src[lane];
+        const double Q = __shfl_sync(0xffffffffu, a.x, 0);
+        const int o = (dyi + 3) * 7 + (dxi + 3);
+        const double* mpw = tab + TL.mpow + (size_t)o * P1 * 2;
+        const double* dnv = tab + TL.dinv + (size_t)o * P1 * 2;
+        // e_k = a_k (-1/D)^k  (k >= 1), e_0 = 0
+        const bool any = Q != 0.0 || (lane >= 1 && (a.x != 0.0 || a.y != 0.0));
+        if (!__any_sync(0xffffffffu, any)) continue;  // empty source box
+        __syncwarp();
+        e[lane] = lane == 0 ? make_double2(0.0, 0.0) : cmul(a, make_double2(mpw[2 * lane], mpw[2 * lane + 1]));
+        __syncwarp();
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 1; k < P1; ++k) s = cfma_r(bc[k], e[k], s);
+        if (lane == 0) {
+          acc.x += s.x + Q * (logh + tab[TL.logd + o]);
+          acc.y += s.y;
+        } else {
+          s.x -= Q * inv_l;
+          acc = cfma(s, make_double2(dnv[2 * lane], dnv[2 * lane + 1]), acc);
+        }
+      }
+    }
+    lp[(lvl_off(l) + b) * P1 + lane] = acc;
+  }
+}
+
 // L2P + P2P: one thread per target inside the root box.  Targets outside
 // are flagged (flag[t] = 1) and summed by the direct kernel.
 template <bool ZERO_CHECK>
