@@ -2316,7 +2316,8 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
                                                      c->f_pxy.as<double2>(), c->f_pq.as<double>());
   // upward pass
   const int wblocks = (int)std::min<int64_t>(nblk(nleaf, kFmmThreads / 32), (int64_t)c->sm_count * 64);
-  k_fmm_p2m<<<std::max(wblocks, 1), kFmmThreads, 0, c->stream>>>(g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(),
+  const size_t sm_p2m = sizeof(double2) * (kFmmThreads / 32) * 32 * (size_t)(P1 | 1);
+  k_fmm_p2m<<<std::max(wblocks, 1), kFmmThreads, sm_p2m, c->stream>>>(g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(),
                                                                   c->f_pxy.as<double2>(), c->f_pq.as<double>(),
                                                                   c->f_mp.as<double2>());
   const size_t P1e = ((size_t)P1 * P1 + 1) & ~(size_t)1;
@@ -2541,7 +2542,8 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
-      cudaFuncSetAttribute(k_fmm_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
+      cudaFuncSetAttribute(k_fmm_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+      cudaFuncSetAttribute(k_fmm_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
     vp_destroy(c);
     return 3;
   }

@@ -152,8 +152,14 @@ __global__ void k_fmm_gather(int64_t S, const int32_t* __restrict__ idx, const d
 __global__ void __launch_bounds__(kFmmThreads)
     k_fmm_p2m(FmmGeom g, const int64_t* __restrict__ beg, const int64_t* __restrict__ end,
               const double2* __restrict__ pxy, const double* __restrict__ pq, double2* __restrict__ mp) {
-  const int lane = threadIdx.x & 31;
+  // lanes own sources while forming q w^k, then own coefficients k: the
+  // 32 x P1 power table goes through shared memory and lane k sums column k
+  // (fixed order), so a batch costs no warp reductions
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = 1 << g.L, P1 = g.p + 1;
+  const int P1s = P1 | 1;  // odd row stride: the lanes' rows fall in different bank groups
+  double2* tab = reinterpret_cast<double2*>(psm) + (size_t)wid * 32 * P1s;  // [source lane][k]
   const int64_t nbox = (int64_t)n * n;
   const double h = g.h0 / n;
   const int64_t base = lvl_off(g.L);
@@ -164,30 +170,41 @@ __global__ void __launch_bounds__(kFmmThreads)
     const int ix = (int)(b % n), iy = (int)(b / n);
     const double cx = g.x0 + (ix + 0.5) * h, cy = g.y0 + (iy + 0.5) * h;
     const double inv_h = 1.0 / h;
-    if (s1 <= s0) {
-      for (int k = lane; k < P1; k += 32) out[k] = make_double2(0.0, 0.0);
-      continue;
-    }
+    double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};  // coefficients lane, lane + 32
     for (int64_t sb = s0; sb < s1; sb += 32) {
       const int64_t s = sb + lane;
       double2 w = make_double2(0.0, 0.0), pw = make_double2(0.0, 0.0);
-      double q = 0.0;
       if (s < s1) {
         const double2 z = pxy[s];
         w = make_double2((z.x - cx) * inv_h, (z.y - cy) * inv_h);
-        q = pq[s];
-        pw = make_double2(q, 0.0);  // q w^0
+        pw = make_double2(pq[s], 0.0);  // q w^0
       }
-      const double Qs = warp_sum(q);
-      if (lane == 0) out[0] = make_double2(sb == s0 ? Qs : out[0].x + Qs, 0.0);
+      __syncwarp();
+      tab[lane * P1s] = pw;
       for (int k = 1; k < P1; ++k) {
         pw = cmul(pw, w);  // q w^k
-        const double re = warp_sum(pw.x), im = warp_sum(pw.y);
-        if (lane == 0) {
-          const double2 prev = sb == s0 ? make_double2(0.0, 0.0) : out[k];
-          out[k] = make_double2(prev.x - re / k, prev.y - im / k);
-        }
+        tab[lane * P1s + k] = pw;
       }
+      __syncwarp();
+      const int nb = (int)min((int64_t)32, s1 - sb);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int k = lane + 32 * r;
+        if (k >= P1) continue;
+        double2 a = acc[r];
+        for (int j = 0; j < nb; ++j) {
+          const double2 v = tab[j * P1s + k];
+          a.x += v.x;
+          a.y += v.y;
+        }
+        acc[r] = a;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int k = lane + 32 * r;
+      if (k >= P1) continue;
+      out[k] = k == 0 ? make_double2(acc[r].x, 0.0) : make_double2(-acc[r].x / k, -acc[r].y / k);
     }
   }
 }
@@ -464,7 +481,23 @@ __global__ void __launch_bounds__(256)
       if (cx < 0 || cx >= n) continue;
       const int64_t c = (int64_t)cy * n + cx;
       const int64_t s1 = end[c];
-      for (int64_t s = beg[c]; s < s1; ++s) {
+      int64_t s = beg[c];
+      // four sources per step: their loads issue together (latency-bound otherwise)
+      for (; s + 4 <= s1; s += 4) {
+        double2 ps[4];
+        double q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ps[i] = pxy[s + i];
+          q[i] = pq[s + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double dx = z.x - ps[i].x, dy = z.y - ps[i].y;
+          sacc = fma(q[i], far_log_r2<ZERO_CHECK>(ltab, laneoff, c3ff, fma(dx, dx, dy * dy)), sacc);
+        }
+      }
+      for (; s < s1; ++s) {
         const double2 ps = pxy[s];
         const double dx = z.x - ps.x, dy = z.y - ps.y;
         sacc = fma(pq[s], far_log_r2<ZERO_CHECK>(ltab, laneoff, c3ff, fma(dx, dx, dy * dy)), sacc);
