@@ -935,6 +935,10 @@ __global__ void __launch_bounds__(PT_WARPS * 32)
 constexpr int SELF_WARPS = 4;
 // dyadic panels per side: N, M <= log2(L / dmin) + 1 <= 45 since dmin >= h > 1e-13 L
 constexpr int kMaxSelfPanels = 128;
+// arc-length nodes evaluate the sigma polynomials by Horner in the monomial
+// basis of x = 2 sigma - 1 up to this order (conditioning (1+sqrt 2)^p <= 1.2e3);
+// the Legendre recurrence above it
+constexpr int kSelfHornerMaxP = 8;
 
 struct SelfGeom {
   double Ax, Ay, ABx, ABy, L, h, st;
@@ -996,6 +1000,9 @@ struct SelfTab {
   double PL[(kMaxPdev + 1) * (kMaxPdev + 1)];  // (2n+1) w_a P_n(2 x_a - 1), [n][a]
   double bt[kMaxPdev + 1], ct[kMaxPdev + 1];   // GGQ-rule moments
   double la[kMaxPdev + 1], lb[kMaxPdev + 1];   // Legendre recurrence (2k+1)/(k+1), k/(k+1)
+  // sigma-direction transform straight to monomials in x = 2 sigma - 1:
+  // PM[j][b] = sum_k [x^j]P_k(x) PL[k][b] (p <= kSelfHornerMaxP: Horner at the nodes)
+  double PM[(kMaxPdev + 1) * (kMaxPdev + 1)];
 };
 
 template <int P>
@@ -1012,7 +1019,8 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   __shared__ double scc[SELF_WARPS][M];
   __shared__ double sV[SELF_WARPS][NP2], sW[SELF_WARPS][NP2], sE[SELF_WARPS][2 * NP];
   __shared__ double sB[SELF_WARPS][kMaxSelfPanels + 1];
-  __shared__ double sPL[NP2], sgx[NP], sbt[NP], sct[NP], sla[NP], slb[NP];
+  constexpr bool kHorner = P <= kSelfHornerMaxP;
+  __shared__ double sPL[NP2], sPM[NP2], sgx[NP], sbt[NP], sct[NP], sla[NP], slb[NP];
   __shared__ double sglx[kMaxGL], sglw[kMaxGL];
   __shared__ double2 sltab[kLogEntries];
   for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
@@ -1021,7 +1029,10 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     sglx[i] = R->gl_x[i];
     sglw[i] = R->gl_w[i];
   }
-  for (int i = threadIdx.x; i < NP2; i += blockDim.x) sPL[i] = ST->PL[i];
+  for (int i = threadIdx.x; i < NP2; i += blockDim.x) {
+    sPL[i] = ST->PL[i];
+    sPM[i] = kHorner ? ST->PM[i] : ST->PL[i];
+  }
   for (int i = threadIdx.x; i < NP; i += blockDim.x) {
     sgx[i] = ST->gx[i];
     sbt[i] = ST->bt[i];
@@ -1107,7 +1118,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         const int n = o / NP, kk = o - n * NP;
         double sum = 0.0;
 #pragma unroll
-        for (int bb = 0; bb < NP; ++bb) sum = fma(sPL[kk * NP + bb], W[n * NP + bb], sum);
+        for (int bb = 0; bb < NP; ++bb) sum = fma(sPM[kk * NP + bb], W[n * NP + bb], sum);
         V[o] = sum;
       }
       __syncwarp();
@@ -1141,19 +1152,31 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         const double ddx = px - tx, ddy = py - ty;
         const double lr0 = 0.5 * fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
         const double x = fma(2.0, sl, -1.0);
-        double q0 = 1.0, q1 = x;
-        double ib = Eb[0], ic = Ec[0];
-        if (NP > 1) {
-          ib = fma(Eb[1], q1, ib);
-          ic = fma(Ec[1], q1, ic);
-        }
+        double ib, ic;
+        if constexpr (kHorner) {
+          ib = Eb[NP - 1];
+          ic = Ec[NP - 1];
 #pragma unroll
-        for (int kk = 1; kk + 1 < NP; ++kk) {
-          const double q2 = fma(sla[kk] * x, q1, -slb[kk] * q0);
-          ib = fma(Eb[kk + 1], q2, ib);
-          ic = fma(Ec[kk + 1], q2, ic);
-          q0 = q1;
-          q1 = q2;
+          for (int kk = NP - 2; kk >= 0; --kk) {
+            ib = fma(ib, x, Eb[kk]);
+            ic = fma(ic, x, Ec[kk]);
+          }
+        } else {
+          double q0 = 1.0, q1 = x;
+          ib = Eb[0];
+          ic = Ec[0];
+          if (NP > 1) {
+            ib = fma(Eb[1], q1, ib);
+            ic = fma(Ec[1], q1, ic);
+          }
+#pragma unroll
+          for (int kk = 1; kk + 1 < NP; ++kk) {
+            const double q2 = fma(sla[kk] * x, q1, -slb[kk] * q0);
+            ib = fma(Eb[kk + 1], q2, ib);
+            ic = fma(Ec[kk + 1], q2, ic);
+            q0 = q1;
+            q1 = q2;
+          }
         }
         acc = fma(ws * G.h, fma(lr0, ib, ic), acc);
       }
@@ -2187,6 +2210,25 @@ int upload_self_tab(vp_ctx* c) {
     T.ct[n] = cc;
     T.la[n] = double(2 * n + 1) / double(n + 1);
     T.lb[n] = double(n) / double(n + 1);
+  }
+  {
+    // monomial coefficients of P_k: mc[k][j] = [x^j] P_k(x), long double recurrence
+    std::vector<long double> mc((size_t)np * np, 0.0L);
+    mc[0] = 1.0L;
+    if (np > 1) mc[1 * np + 1] = 1.0L;
+    for (int k = 1; k + 1 < np; ++k)
+      for (int j = 0; j < np; ++j) {
+        long double v = -(long double)k * mc[(size_t)(k - 1) * np + j];
+        if (j > 0) v += (long double)(2 * k + 1) * mc[(size_t)k * np + j - 1];
+        mc[(size_t)(k + 1) * np + j] = v / (long double)(k + 1);
+      }
+    for (int j = 0; j < np; ++j)
+      for (int a = 0; a < np; ++a) {
+        long double v = 0.0L;
+        for (int k = 0; k < np; ++k)
+          v += mc[(size_t)k * np + j] * (long double)(2 * k + 1) * (0.5L * gw[a]) * (long double)legendre(k, gx[a]);
+        T.PM[j * np + a] = (double)v;
+      }
   }
   CUDA_TRY(c, c->d_selftab.ensure(sizeof(SelfTab)));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_selftab.p, &T, sizeof(SelfTab), cudaMemcpyHostToDevice, c->stream));
