@@ -15,6 +15,8 @@ ap.add_argument("--q", type=int, default=0)
 ap.add_argument("--far", default="fmm")
 ap.add_argument("--check", type=int, default=400)
 ap.add_argument("--out", default="")
+ap.add_argument("--cache-depth", type=int, default=-2, help="near cache max depth (-2: library default)")
+ap.add_argument("--cache-gb", type=float, default=0.0, help="near cache byte budget in GB (0: default)")
 a = ap.parse_args()
 t0 = time.time()
 pr = vp.load_config(a.config, a.q)
@@ -22,6 +24,8 @@ gen = time.time() - t0
 with vp.Evaluator(0) as ev:
     ev.load(pr)
     ev.set_far_method(a.far)
+    if a.cache_depth != -2 or a.cache_gb > 0:
+        ev.set_near_cache(a.cache_depth if a.cache_depth != -2 else 3, int(a.cache_gb * (1 << 30)))
     ev.evaluate(pr.txy)  # warm-up at full size: device buffers allocated outside the timed pass
     t1 = time.time()
     u, st = ev.evaluate(pr.txy)
