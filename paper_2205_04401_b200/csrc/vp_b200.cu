@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
           if (k + 1 < K || nok[k]) {
             const double dx = fma(-nu[k], dd.z, fma(-nv[k], cc.x, dd.x));
             const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
-            acc = fma(g[k], far_log_r2<false>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
+            acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
           }
         }
       }

@@ -249,7 +249,25 @@ inline void log_table_fill(double2* host /* kLogEntries */) {
 //   8 bits: Taylor degree 5 (truncation 9e-18);
 //   9 bits: minimax degree 4 on [-2^-10, 2^-10] (max error 2.3e-17).
 static_assert(kLogBits == 8 || kLogBits == 9, "log table: 8 or 9 index bits");
+// The 9-bit polynomial's constants and ln 2 live in __constant__ memory so a
+// DFMA takes them as a constant-bank operand: literal doubles are otherwise
+// re-materialised into uniform registers inside register-tight loops.
+// (CB = true; K2 keeps literals, which measure 0.5 % faster there.)
+__constant__ double c_logk[4] = {-0.25000024181904215854, 0.3333334991010435487, -0.49999999999992096269,
+                                 0.69314718055994530942};
+template <bool CB>
+__device__ __forceinline__ double log_ln2() {
+  if constexpr (CB) return c_logk[3];
+  return 0.69314718055994530942;
+}
+template <bool CB = true>
 __device__ __forceinline__ double log1p_poly(double t, double L) {
+  if constexpr (kLogBits == 9 && CB) {
+    double i = fma(t, c_logk[0], c_logk[1]);
+    i = fma(t, i, c_logk[2]);
+    i = fma(t, i, 1.0);
+    return fma(t, i, L);
+  }
   if constexpr (kLogBits == 8) {
     double i = fma(t, 0.2, -0.25);
     i = fma(t, i, 0.33333333333333333);
@@ -281,8 +299,8 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double ed = log_exponent((unsigned)hi);
   const double t = fma(m, tb.x, -1.0);
-  const double p = log1p_poly(t, tb.y);
-  const double lg = fma(ed, 0.69314718055994530942, p);
+  const double p = log1p_poly<true>(t, tb.y);
+  const double lg = fma(ed, log_ln2<true>(), p);
   if constexpr (ZERO_CHECK) return hi >= 0x00100000 ? lg : 0.0;
   return lg;
 }
@@ -298,7 +316,7 @@ __device__ __forceinline__ double fast_log_r2(const double2* __restrict__ base, 
 //     its own element S(t), whose point sum is subtracted again with the same
 //     function (subtract-and-add), so the finite value
 //     returned for r^2 == 0 cancels.
-template <bool ZERO_CHECK>
+template <bool ZERO_CHECK, bool CB = false>
 __device__ __forceinline__ double far_log_r2(const double2* tab, unsigned laneoff, unsigned c3ff, double x) {
   const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
   unsigned off, mhi;
@@ -310,8 +328,8 @@ __device__ __forceinline__ double far_log_r2(const double2* tab, unsigned laneof
   const double m = __hiloint2double((int)mhi, (int)lo);
   const double ed = log_exponent(hi);
   const double t = fma(m, tb.x, -1.0);
-  const double p = log1p_poly(t, tb.y);
-  const double lg = fma(ed, 0.69314718055994530942, p);
+  const double p = log1p_poly<CB>(t, tb.y);
+  const double lg = fma(ed, log_ln2<CB>(), p);
   if constexpr (ZERO_CHECK) return hi >= 0x00100000u ? lg : 0.0;
   return lg;
 }
