@@ -18,7 +18,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cub/cub.cuh>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "vp.h"
@@ -1730,6 +1732,12 @@ struct vp_ctx {
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
+  // far field on its own stream and host thread when it overlaps the near and
+  // self stages (FMM); fs is the stream the far-path functions use
+  cudaStream_t s2 = nullptr, fs = nullptr;
+  std::mutex err_mu;
+  DevBuf f_tmp;
+  int far_launches = 0;
   // curved (blending-map) elements, SURVEY.md §8(f3)
   int curve_deg = 0;
   std::vector<int32_t> h_ecurve, h_celist;
@@ -1740,7 +1748,10 @@ struct vp_ctx {
 namespace {
 
 int set_err(vp_ctx* c, int code, const std::string& m) {
-  if (c) c->err = m;
+  if (c) {
+    std::lock_guard<std::mutex> lk(c->err_mu);
+    c->err = m;
+  }
   return code;
 }
 
@@ -2273,6 +2284,8 @@ constexpr size_t kFarSmem = sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeo
 int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check, DevBuf& part);
 int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check);
 
+// the far field on stream c->fs (c->stream unless the caller overlaps it);
+// its launches are counted in c->far_launches
 int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check) {
   if (c->far_method == 1) return fmm_far_sum(c, T, txy, ufar, zero_check);
   return direct_far_sum(c, T, txy, ufar, zero_check, c->d_part);
@@ -2290,16 +2303,16 @@ int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool 
   CUDA_TRY(c, part.ensure(sizeof(double) * T * nsplit));
   dim3 grid((unsigned)tblocks, (unsigned)nsplit);
   if (zero_check)
-    k_far<true><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+    k_far<true><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
                                                           c->d_sq.as<double>(), chunk, part.as<double>(),
                                                           0x3ff00000u);
   else
-    k_far<false><<<grid, FAR_THREADS, kFarSmem, c->stream>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+    k_far<false><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
                                                            c->d_sq.as<double>(), chunk, part.as<double>(),
                                                            0x3ff00000u);
-  k_far_reduce<<<nblk(T, 256), 256, 0, c->stream>>>(T, nsplit, part.as<double>(), ufar);
+  k_far_reduce<<<nblk(T, 256), 256, 0, c->fs>>>(T, nsplit, part.as<double>(), ufar);
   CUDA_TRY(c, cudaGetLastError());
-  c->last_launches += 2;
+  c->far_launches += 2;
   return 0;
 }
 
@@ -2326,8 +2339,8 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
     fmm_tables_fill(p, tab);
     CUDA_TRY(c, c->f_tab.ensure(sizeof(double) * tab.size()));
     CUDA_TRY(c, cudaMemcpyAsync(c->f_tab.p, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice,
-                                c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+                                c->fs));
+    CUDA_TRY(c, cudaStreamSynchronize(c->fs));
     c->tab_p = p;
   }
   // bin and sort the sources by leaf box (stable: source order kept within a box)
@@ -2341,25 +2354,25 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   CUDA_TRY(c, c->f_pq.ensure(sizeof(double) * S));
   CUDA_TRY(c, c->f_mp.ensure(sizeof(double2) * nbox * P1));
   CUDA_TRY(c, c->f_lp.ensure(sizeof(double2) * nbox * P1));
-  k_fmm_keys<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->d_sx.as<double>(), c->d_sy.as<double>(), g,
+  k_fmm_keys<<<nblk(S, 256), 256, 0, c->fs>>>(S, c->d_sx.as<double>(), c->d_sy.as<double>(), g,
                                                    c->f_keys.as<int32_t>(), c->f_vals.as<int32_t>());
   size_t tmpb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmpb, c->f_keys.as<int32_t>(), c->f_keys2.as<int32_t>(),
-                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->stream);
-  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
-  cub::DeviceRadixSort::SortPairs(c->d_tmp.p, tmpb, c->f_keys.as<int32_t>(), c->f_keys2.as<int32_t>(),
-                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->stream);
-  CUDA_TRY(c, cudaMemsetAsync(c->f_beg.p, 0, sizeof(int64_t) * nleaf, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->f_end.p, 0, sizeof(int64_t) * nleaf, c->stream));
-  k_cell_ranges<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->f_keys2.as<int32_t>(), c->f_beg.as<int64_t>(),
+                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->fs);
+  CUDA_TRY(c, c->f_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->f_tmp.p, tmpb, c->f_keys.as<int32_t>(), c->f_keys2.as<int32_t>(),
+                                  c->f_vals.as<int32_t>(), c->f_idx.as<int32_t>(), (int)S, 0, 2 * L, c->fs);
+  CUDA_TRY(c, cudaMemsetAsync(c->f_beg.p, 0, sizeof(int64_t) * nleaf, c->fs));
+  CUDA_TRY(c, cudaMemsetAsync(c->f_end.p, 0, sizeof(int64_t) * nleaf, c->fs));
+  k_cell_ranges<<<nblk(S, 256), 256, 0, c->fs>>>(S, c->f_keys2.as<int32_t>(), c->f_beg.as<int64_t>(),
                                                       c->f_end.as<int64_t>());
-  k_fmm_gather<<<nblk(S, 256), 256, 0, c->stream>>>(S, c->f_idx.as<int32_t>(), c->d_sx.as<double>(),
+  k_fmm_gather<<<nblk(S, 256), 256, 0, c->fs>>>(S, c->f_idx.as<int32_t>(), c->d_sx.as<double>(),
                                                      c->d_sy.as<double>(), c->d_sq.as<double>(),
                                                      c->f_pxy.as<double2>(), c->f_pq.as<double>());
   // upward pass
   const int wblocks = (int)std::min<int64_t>(nblk(nleaf, kFmmThreads / 32), (int64_t)c->sm_count * 64);
   const size_t sm_p2m = sizeof(double2) * (kFmmThreads / 32) * 32 * (size_t)(P1 | 1);
-  k_fmm_p2m<<<std::max(wblocks, 1), kFmmThreads, sm_p2m, c->stream>>>(g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(),
+  k_fmm_p2m<<<std::max(wblocks, 1), kFmmThreads, sm_p2m, c->fs>>>(g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(),
                                                                   c->f_pxy.as<double2>(), c->f_pq.as<double>(),
                                                                   c->f_mp.as<double2>());
   const size_t P1e = ((size_t)P1 * P1 + 1) & ~(size_t)1;
@@ -2367,7 +2380,7 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   for (int l = L - 1; l >= 2; --l) {
     const int64_t nb = 1ll << (2 * l);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
-    k_fmm_m2m<<<blocks, kFmmThreads, sm_m2m, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>());
+    k_fmm_m2m<<<blocks, kFmmThreads, sm_m2m, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>());
   }
   // downward pass
   const size_t sm_m2l = sizeof(double) * (2 * P1e + 8 * P1 + 2 * (kFmmThreads / 32) * P1);
@@ -2375,48 +2388,48 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
     const int64_t nb = 1ll << (2 * l);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
     if (P1 == 32)
-      k_fmm_m2l32<<<blocks, kFmmThreads, 0, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+      k_fmm_m2l32<<<blocks, kFmmThreads, 0, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
                                                           c->f_lp.as<double2>());
     else
-      k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->stream>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+      k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
                                                             c->f_lp.as<double2>());
   }
   // L2P + P2P
   CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
   const size_t sm_eval = sizeof(LogTab);
   if (zero_check)
-    k_fmm_eval<true><<<nblk(T, 256), 256, sm_eval, c->stream>>>(
+    k_fmm_eval<true><<<nblk(T, 256), 256, sm_eval, c->fs>>>(
         T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
         c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
   else
-    k_fmm_eval<false><<<nblk(T, 256), 256, sm_eval, c->stream>>>(
+    k_fmm_eval<false><<<nblk(T, 256), 256, sm_eval, c->fs>>>(
         T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
         c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
   CUDA_TRY(c, cudaGetLastError());
-  c->last_launches += 7 + 2 * (L - 1);
+  c->far_launches += 7 + 2 * (L - 1);
   // targets outside the root box: direct far sum
   CUDA_TRY(c, c->f_oidx.ensure(sizeof(int32_t) * (T + 1)));
   CUDA_TRY(c, c->f_cnt.ensure(sizeof(int64_t)));
   tmpb = 0;
   cub::CountingInputIterator<int32_t> it(0);
   cub::DeviceSelect::Flagged(nullptr, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
-                             c->f_cnt.as<int64_t>(), (int)T, c->stream);
-  CUDA_TRY(c, c->d_tmp.ensure(tmpb));
-  cub::DeviceSelect::Flagged(c->d_tmp.p, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
-                             c->f_cnt.as<int64_t>(), (int)T, c->stream);
+                             c->f_cnt.as<int64_t>(), (int)T, c->fs);
+  CUDA_TRY(c, c->f_tmp.ensure(tmpb));
+  cub::DeviceSelect::Flagged(c->f_tmp.p, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
+                             c->f_cnt.as<int64_t>(), (int)T, c->fs);
   int64_t nout = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&nout, c->f_cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&nout, c->f_cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->fs));
+  CUDA_TRY(c, cudaStreamSynchronize(c->fs));
   c->fmm_outside = nout;
   if (nout > 0) {
     CUDA_TRY(c, c->f_otxy.ensure(sizeof(double2) * nout));
     CUDA_TRY(c, c->f_ou.ensure(sizeof(double) * nout));
-    k_gather_targets<<<nblk(nout, 256), 256, 0, c->stream>>>(nout, c->f_oidx.as<int32_t>(), txy,
+    k_gather_targets<<<nblk(nout, 256), 256, 0, c->fs>>>(nout, c->f_oidx.as<int32_t>(), txy,
                                                               c->f_otxy.as<double2>());
     if (int rc = direct_far_sum(c, nout, c->f_otxy.as<double2>(), c->f_ou.as<double>(), zero_check, c->d_part))
       return rc;
-    k_scatter_add<<<nblk(nout, 256), 256, 0, c->stream>>>(nout, c->f_oidx.as<int32_t>(), c->f_ou.as<double>(), ufar);
-    c->last_launches += 2;
+    k_scatter_add<<<nblk(nout, 256), 256, 0, c->fs>>>(nout, c->f_oidx.as<int32_t>(), c->f_ou.as<double>(), ufar);
+    c->far_launches += 2;
   }
   return 0;
 }
@@ -2467,8 +2480,34 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   if (int rc = compute_sources(c)) return rc;
   CUDA_TRY(c, cudaEventRecord(ev[6], c->stream));
   CUDA_TRY(c, c->d_ufar.ensure(sizeof(double) * (T + 1)));
-  if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false)) return rc;
-  CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+  c->far_launches = 0;
+  // FMM: the far field overlaps the near and self stages, on its own stream
+  // and host thread (its host syncs then wait on that stream only).  The
+  // direct K2 fills every SM by itself, so it runs alone and its per-kernel
+  // timing stays clean.
+  const bool overlap = c->far_method == 1;
+  int far_rc = 0;
+  std::thread far_thread;
+  struct FarJoin {  // joins on every return path and restores the far stream
+    vp_ctx* c;
+    std::thread& t;
+    ~FarJoin() {
+      if (t.joinable()) t.join();
+      c->fs = c->stream;
+    }
+  } far_join{c, far_thread};
+  if (overlap) {
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, ev[6], 0));
+    c->fs = c->s2;
+    far_thread = std::thread([c, T, txy, &far_rc] {
+      cudaSetDevice(c->device);
+      far_rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false);
+      if (!far_rc && cudaEventRecord(c->ev[2], c->s2) != cudaSuccess) far_rc = set_err(c, 3, "cuda: far event");
+    });
+  } else {
+    if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false)) return rc;
+    CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
+  }
   CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * (n_ids + 1)));
   CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * (n_ids + 1)));
   if (n_ids > 0) {
@@ -2483,6 +2522,11 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
                 nullptr, nullptr);
   c->last_launches += 1;
   CUDA_TRY(c, cudaEventRecord(ev[4], c->stream));
+  if (far_thread.joinable()) far_thread.join();
+  c->fs = c->stream;
+  if (far_rc) return far_rc;
+  c->last_launches += c->far_launches;
+  if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2], 0));
   CUDA_TRY(c, c->d_psum.ensure(sizeof(double) * (T + 1)));
   k_psum_tgt<<<(unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64), PT_WARPS * 32, 0,
                c->stream>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
@@ -2527,7 +2571,9 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     st->t_sources_ms = msrc;
     st->t_far_kernel_ms = mfar;
     st->t_far_ms = ms[1];
-    st->t_near_ms = ms[2];
+    float mnear = ms[2];
+    if (overlap) cudaEventElapsedTime(&mnear, ev[6], ev[3]);  // near starts with the far field
+    st->t_near_ms = mnear;
     st->t_self_ms = ms[3];
     float tot = 0;
     cudaEventElapsedTime(&tot, ev[0], ev[5]);
@@ -2560,10 +2606,12 @@ int vp_create(int device, vp_ctx** out) {
   vp_ctx* c = new vp_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return 3;
   }
+  c->fs = c->stream;
   for (auto& e : c->ev) cudaEventCreate(&e);
   double cn[kMaxModes];
   for (int n2 = 0; n2 <= kMaxPdev; ++n2)
@@ -2613,6 +2661,7 @@ void vp_destroy(vp_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->s2) cudaStreamDestroy(c->s2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
