@@ -187,9 +187,14 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
                         const int32_t* __restrict__ celems, const int32_t* __restrict__ allnear,
                         int n_allnear, int32_t* __restrict__ self_out,
                         int64_t* __restrict__ cnt_out, const int64_t* __restrict__ off,
-                        int32_t* __restrict__ ids, double2* __restrict__ self_ref, CurvesDev CV) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
+                        int32_t* __restrict__ ids, double2* __restrict__ self_ref, CurvesDev CV,
+                        const int32_t* __restrict__ tlist, int32_t* __restrict__ scratch, int cap,
+                        int32_t* __restrict__ over, unsigned* __restrict__ n_over) {
+  // count pass: also keeps the first `cap` ids of N(t) in scratch[t * cap ..]
+  // and lists the targets with more (walked again by the fill pass over tlist)
+  const int64_t ti = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ti >= T) return;
+  const int64_t t = tlist ? tlist[ti] : ti;
   const double2 p = txy[t];
   const double tx = p.x, ty = p.y;
   int64_t b = 0, e = 0;
@@ -231,6 +236,7 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
     }
     if (rn_in_near(R, tx, ty)) {
       if (FILL) ids[o++] = id;
+      else if (n < cap) scratch[t * cap + n] = id;
       ++n;
     }
   }
@@ -238,7 +244,17 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
     cnt_out[t] = n;
     self_out[t] = self;
     if (self_ref) self_ref[t] = make_double2(sxi, seta);
+    if (n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)t;
   }
+}
+
+__global__ void k_lists_copy(int64_t T, const int64_t* __restrict__ off, int cap,
+                             const int32_t* __restrict__ scratch, int32_t* __restrict__ ids) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int64_t o = off[t], n = off[t + 1] - o;
+  if (n > cap) return;
+  for (int64_t i = 0; i < n; ++i) ids[o + i] = scratch[t * cap + i];
 }
 
 __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* __restrict__ pt) {
@@ -1728,6 +1744,7 @@ struct vp_ctx {
   int64_t cache_max_bytes = 12ll << 30;
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
   DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
+  DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
@@ -2030,8 +2047,12 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_loffc.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_loffd.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_ldeep.ensure(sizeof(int32_t) * (n + 1)));
-  // scratch for the first `cap` leaves of every pair, within a memory budget
-  const int cap = (int)std::min<int64_t>(64, (c->leaf_scratch_budget / 8) / std::max<int64_t>(n, 1));
+  // scratch for the first `cap` leaves of every pair, within a memory budget:
+  // the larger of leaf_scratch_budget and 10 % of the free device memory
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+  const int64_t budget = std::max<int64_t>(c->leaf_scratch_budget, (int64_t)(free_b / 10));
+  const int cap = (int)std::min<int64_t>(64, (budget / 8) / std::max<int64_t>(n, 1));
   CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
   CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
@@ -2440,27 +2461,38 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   CUDA_TRY(c, c->d_cnt.ensure(sizeof(int64_t) * (T + 1)));
   CUDA_TRY(c, c->d_off.ensure(sizeof(int64_t) * (T + 1)));
   CUDA_TRY(c, c->d_selfref.ensure(sizeof(double2) * (T + 1)));
+  const int cap = 16;  // N(t) ids kept by the count pass (|N(t)| ~ 1-7 on the configs)
+  CUDA_TRY(c, c->d_lsc.ensure(sizeof(int32_t) * (size_t)T * cap + 4));
+  CUDA_TRY(c, c->d_tover.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->d_ntover.ensure(sizeof(unsigned)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_ntover.p, 0, sizeof(unsigned), c->stream));
   const GridDev G = c->grid;
   const int nan = (int)c->h_allnear.size();
   k_lists<false><<<nblk(T, 128), 128, 0, c->stream>>>(
       T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
-      c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c));
+      c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c), nullptr,
+      c->d_lsc.as<int32_t>(), cap, c->d_tover.as<int32_t>(), c->d_ntover.as<unsigned>());
   CUDA_TRY(c, cudaMemsetAsync(c->d_cnt.as<int64_t>() + T, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
   CUDA_TRY(c, c->d_tmp.ensure(tmpb));
   cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
   int64_t n_ids = 0;
+  unsigned nover = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&n_ids, c->d_off.as<int64_t>() + T, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&nover, c->d_ntover.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   CUDA_TRY(c, c->d_ids.ensure(sizeof(int32_t) * (n_ids + 1)));
-  k_lists<true><<<nblk(T, 128), 128, 0, c->stream>>>(
-      T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
-      c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr,
-      c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), nullptr, curves_dev(c));
+  k_lists_copy<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), cap, c->d_lsc.as<int32_t>(),
+                                                    c->d_ids.as<int32_t>());
+  if (nover > 0)
+    k_lists<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
+        nover, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
+        c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr, c->d_off.as<int64_t>(),
+        c->d_ids.as<int32_t>(), nullptr, curves_dev(c), c->d_tover.as<int32_t>(), nullptr, 0, nullptr, nullptr);
   CUDA_TRY(c, cudaGetLastError());
-  c->last_launches += 3;
+  c->last_launches += 3 + (nover > 0 ? 1 : 0);
   *n_ids_out = n_ids;
   return 0;
 }
