@@ -883,6 +883,105 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
   }
 }
 
+// K4b cached leaves, evaluation form: one warp per TARGET.  The cached leaves
+// of t's pairs are contiguous in the CSR array, so the warp walks them in
+// 32-leaf batches across pair boundaries (a lane finds its leaf's pair among
+// t's few pairs); the target and the per-pair index loads are paid once per
+// target, not per pair.  Writes the per-target sum part_t[t] (k_assemble adds
+// it); the per-pair API keeps k_near_c.
+template <int K>
+__global__ void __launch_bounds__(NC_WARPS * 32, 2)
+    k_near_ct(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
+              const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
+              const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
+              const double* __restrict__ gcache, const double* __restrict__ slot_ref, int cache_depth,
+              double* __restrict__ part_t, unsigned c3ff) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
+  __shared__ double4 sD[NC_WARPS][32];
+  __shared__ double2 sC[NC_WARPS][32];
+  __shared__ long long sgo[NC_WARPS][32];  // cache row offset of each leaf
+  const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
+  const int Ln = R->len_n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nu[K], nv[K];
+  bool nok[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int n = lane + 32 * k;
+    nok[k] = n < Ln;
+    nu[k] = nok[k] ? R->near_x[n] : 0.0;
+    nv[k] = nok[k] ? R->near_y[n] : 0.0;
+  }
+  __syncthreads();
+  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  const double* gl = gcache + lane;
+  for (int64_t t = (int64_t)blockIdx.x * NC_WARPS + wid; t < T; t += (int64_t)gridDim.x * NC_WARPS) {
+    const int64_t q0 = toff[t], q1 = toff[t + 1];
+    double acc = 0.0;
+    if (q1 > q0) {
+      const int64_t L0 = loff[q0], L1 = loff[q1];
+      const double2 tp = txy[t];
+      const double tx = tp.x, ty = tp.y;
+      int64_t q = q0;  // this lane's current pair (leaves ascend with the lane's batches)
+      for (int64_t lb = L0; lb < L1; lb += 32) {
+        const int nb = (int)min((int64_t)32, L1 - lb);
+        __syncwarp();
+        if (lane < nb) {
+          const int64_t Lf = lb + lane;
+          while (loff[q + 1] <= Lf) ++q;
+          const int32_t e = pair_elem[q];
+          const unsigned long long code = leaves[Lf];
+          const int d = (int)(code >> 58);
+          const ElemRec& Er = el[e];
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const double* r = slot_ref + 6 * slot;
+          const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
+          const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
+          sD[wid][lane] = make_double4(tx - pax, ty - pay, fma(r[3], Er.e2x, r[2] * Er.e1x),
+                                       fma(r[3], Er.e2y, r[2] * Er.e1y));
+          sC[wid][lane] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
+          sgo[wid][lane] = ((long long)e * nslot + slot) * Ln;
+        }
+        __syncwarp();
+        double gn[K], gm[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          gn[k] = nok[k] ? __ldg(gl + sgo[wid][0] + 32 * k) : 0.0;
+          gm[k] = nok[k] && nb > 1 ? __ldg(gl + sgo[wid][1] + 32 * k) : 0.0;
+        }
+#pragma unroll 1
+        for (int li = 0; li < nb; ++li) {
+          double g[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            g[k] = gn[k];
+            gn[k] = gm[k];
+          }
+          if (li + 2 < nb) {
+            const long long sn = sgo[wid][li + 2];
+#pragma unroll
+            for (int k = 0; k < K; ++k) gm[k] = nok[k] ? __ldg(gl + sn + 32 * k) : 0.0;
+          }
+          const double4 dd = sD[wid][li];
+          const double2 cc = sC[wid][li];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k + 1 < K || nok[k]) {
+              const double dx = fma(-nu[k], dd.z, fma(-nv[k], cc.x, dd.x));
+              const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
+              acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
+            }
+          }
+        }
+      }
+    }
+    const double val = warp_sum(acc);
+    if (lane == 0) part_t[t] = val;
+  }
+}
+
 // Point sums of subtract-and-add for the per-pair API: part_s[p] =
 // sum_{i in T} q_i log r_{t,i}^2 (coincident pairs exactly 0);
 // warp per pair, lanes over T's sources.
@@ -1626,13 +1725,16 @@ __global__ void __launch_bounds__(128)
   out[i] = density<P>(cc, xi, eta);
 }
 
-// u = (u_far - psum) + sum of near values + self value
+// u = (u_far - psum) + near (cached leaves, per target) + sum of the other
+// near values (per pair) + self value
 __global__ void k_assemble(int64_t T, const double* __restrict__ ufar, const double* __restrict__ psum,
-                           const int64_t* __restrict__ off, const double* __restrict__ corr,
-                           const double* __restrict__ corr_self, double* __restrict__ u) {
+                           const double* __restrict__ neart, const int64_t* __restrict__ off,
+                           const double* __restrict__ corr, const double* __restrict__ corr_self,
+                           double* __restrict__ u) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   double s = ufar[t] - psum[t];
+  if (off[t + 1] > off[t]) s += neart[t];
   for (int64_t p = off[t]; p < off[t + 1]; ++p) s += corr[p];
   s += corr_self[t];
   u[t] = s;
@@ -1745,6 +1847,7 @@ struct vp_ctx {
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
   DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
   DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
+  DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
@@ -1986,6 +2089,16 @@ void launch_near_c(vp_ctx* c, int blocks, int64_t n, const int32_t* ptgt, const 
       c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, c->d_npa.as<double>(), 0x3ff00000u);
 }
 
+template <int K>
+void launch_near_ct(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
+                    const double* gc) {
+  const int blocks = (int)std::min<int64_t>(nblk(T, NC_WARPS), (int64_t)c->sm_count * 16);
+  k_near_ct<K><<<std::max(blocks, 1), NC_WARPS * 32, sizeof(LogTab), c->stream>>>(
+      T, toff, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
+      c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, c->d_neart.as<double>(),
+      0x3ff00000u);
+}
+
 #define VP_DISPATCH_K(k, F, ...)     \
   switch (k) {                       \
     case 1: F<1>(__VA_ARGS__); break; \
@@ -2000,7 +2113,7 @@ void launch_near_c(vp_ctx* c, int blocks, int64_t n, const int32_t* ptgt, const 
 
 template <int P>
 void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
-                     double* corr, double* sub, int64_t ndeep) {
+                     double* corr, double* sub, int64_t ndeep, int64_t T, const int64_t* toff) {
   const int blocks = (int)std::min<int64_t>(nblk(ndeep, NEAR_WARPS), (int64_t)c->sm_count * 32);
   const double* gc = c->cache_depth >= 0 ? c->d_gcache.as<double>() : nullptr;
   const int cblocks = (int)std::min<int64_t>(nblk(n, NC_WARPS), (int64_t)c->sm_count * 16);
@@ -2008,7 +2121,10 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
     k_point_sum<<<(unsigned)std::min<int64_t>(nblk(n, PS_WARPS), (int64_t)c->sm_count * 64), PS_WARPS * 32, 0,
                   c->stream>>>(n, ptgt, pelem, txy, c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(),
                                c->d_sq.as<double>(), c->d_nps.as<double>(), true);
-  if (c->cache_depth >= 0) {
+  if (c->cache_depth >= 0 && toff) {  // evaluation: per-target sums of the cached leaves
+    cudaMemsetAsync(c->d_npa.p, 0, sizeof(double) * n, c->stream);
+    VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_ct, c, T, toff, pelem, txy, gc);
+  } else if (c->cache_depth >= 0) {
     VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_c, c, cblocks, n, ptgt, pelem, txy, gc);
   } else {
     cudaMemsetAsync(c->d_npa.p, 0, sizeof(double) * n, c->stream);
@@ -2038,8 +2154,10 @@ void launch_near_curved(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t
 int build_near_cache(vp_ctx* c);
 void decide_cache_depth(vp_ctx* c);
 
+// T/toff: the evaluation's targets and pair CSR (cached leaves then summed per
+// target into d_neart); nullptr for the per-pair API
 int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem, const double2* txy,
-                double* corr, double* sub, int64_t* leaves_host) {
+                double* corr, double* sub, int64_t* leaves_host, int64_t T = 0, const int64_t* toff = nullptr) {
   decide_cache_depth(c);
   CUDA_TRY(c, c->d_lcnt.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_lcntc.ensure(sizeof(int64_t) * (n + 1)));
@@ -2097,7 +2215,11 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
-  VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub, (int64_t)ndeep);
+  if (toff) {
+    CUDA_TRY(c, c->d_neart.ensure(sizeof(double) * (T + 1)));
+    if (c->cache_depth < 0) CUDA_TRY(c, cudaMemsetAsync(c->d_neart.p, 0, sizeof(double) * T, c->stream));
+  }
+  VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub, (int64_t)ndeep, T, toff);
   if (has_curves(c)) {
     VP_DISPATCH_P(c->p, launch_near_curved, c, n, ptgt, pelem, txy, corr, sub);
     c->last_launches += 1;
@@ -2546,7 +2668,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     k_pair_tgt<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), c->d_ptgt.as<int32_t>());
     c->last_launches += 1;
     if (int rc = launch_near(c, n_ids, c->d_ptgt.as<int32_t>(), c->d_ids.as<int32_t>(), txy,
-                             c->d_corr.as<double>(), nullptr, nullptr)) return rc;
+                             c->d_corr.as<double>(), nullptr, nullptr, T, c->d_off.as<int64_t>())) return rc;
   }
   CUDA_TRY(c, cudaEventRecord(ev[3], c->stream));
   CUDA_TRY(c, c->d_corr_self.ensure(sizeof(double) * (T + 1)));
@@ -2564,9 +2686,10 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
                c->stream>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
                             c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
                             c->d_psum.as<double>());
+  CUDA_TRY(c, c->d_neart.ensure(sizeof(double) * (T + 1)));
   k_assemble<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_ufar.as<double>(), c->d_psum.as<double>(),
-                                                   c->d_off.as<int64_t>(), c->d_corr.as<double>(),
-                                                   c->d_corr_self.as<double>(), u);
+                                                   c->d_neart.as<double>(), c->d_off.as<int64_t>(),
+                                                   c->d_corr.as<double>(), c->d_corr_self.as<double>(), u);
   k_count_self<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_self.as<int32_t>(), c->d_stats.as<unsigned long long>());
   c->last_launches += 3;
   CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
@@ -2654,13 +2777,21 @@ int vp_create(int device, vp_ctx** out) {
     return 3;
   }
   if (cudaFuncSetAttribute(k_near_c<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_ct<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
