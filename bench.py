@@ -35,11 +35,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 # Algorithmic work of one far pair as formulated on B200:
-# dx, dy (2 DADD), r^2 (DMUL + DFMA), log r^2 (6 DFMA: t, 4-term polynomial,
-# exponent), accumulate (1 DFMA) = 11 FP64 operations = 8 FMA (2 flops) +
-# 3 add/mul (1 flop) = 19 flops.  (The exponent's int->double conversion runs
-# on the XU pipe.)
-FAR_FLOP_PER_PAIR = 19
+# dx, dy (2 DADD), r^2 (DMUL + DFMA), log r^2 (5 DFMA: t, 3-term polynomial
+# on the 10-bit table, exponent), accumulate (1 DFMA) = 10 FP64 operations =
+# 7 FMA (2 flops) + 3 add/mul (1 flop) = 17 flops.  (The exponent's
+# int->double conversion runs on the XU pipe.)  The ncu SASS counters of K2
+# (profiles/r01_fp64_flops_config2.json) must agree: flop_per_pair_ncu.
+FAR_FLOP_PER_PAIR = 17
+FP64_FLOPS_PROFILE = os.path.join(HERE, "profiles", "r01_fp64_flops_config2.json")
 # SURVEY.md §8(d)'s frozen figure counted the libdevice log (51 flops/pair);
 # reported beside the roofline for comparison.
 SURVEY_FAR_FLOP_PER_PAIR = 51
@@ -93,8 +95,9 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (host time, fields)
         self.proc = None
+        self.window = None
 
     def start(self):
         try:
@@ -109,7 +112,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def wait_first(self, timeout=10.0):
+        """nvidia-smi's start-up (NVML init) can stall CUDA calls of this
+        process, so it is started before the warm-up and the timed region
+        begins only after its first sample."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def stop(self):
         if self.proc is None:
@@ -121,6 +135,11 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.th.join(timeout=1)
+        if self.window is not None:  # samples taken during the timed region (+ one period)
+            a, b = self.window
+            inside = [r for r in self.rows if a - 0.1 <= r[0] <= b + 0.1]
+            self.rows = inside or self.rows[-1:]
+        self.rows = [r[1] for r in self.rows]
         sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -223,12 +242,14 @@ def main():
             dist.all_gather_into_tensor(gathered, d_u)
         return st
 
+    clk = ClockSampler(local)
+    clk.start()
+    clk.wait_first()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     # ---- timed region: K device-timed steps, L2 flushed between steps ----
-    clk = ClockSampler(local)
-    clk.start()
+    host_t0 = time.perf_counter()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stats = []
@@ -243,6 +264,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    clk.mark(host_t0, time.perf_counter())
     clocks = clk.stop()
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_total = float(sum(ms_steps))
@@ -335,6 +357,25 @@ def main():
                "sample": f"every {args.cpu_stride}th target of config {pr.config} ({n} of {pr.n_tgt}), "
                          f"full far+near+self per target, oracle/liboracle.so OpenMP, {dt:.1f} s"}
 
+    # near field (K4 + K5 stages): executed FP64 flops per step from the ncu
+    # SASS counters of the same configuration (deterministic work), over the
+    # live device time of those stages
+    roof_near = None
+    prof_fl = load_json(FP64_FLOPS_PROFILE)
+    if prof_fl and pr.config == 2 and not args.q and args.seed == 0 and not prof_fl.get("config_args"):
+        nf = float(prof_fl["near_stage_fp64_flops"])
+        ach = nf / (pair_ms * 1e-3) / 1e12
+        kf = prof_fl["kernels"].get("k_far<0>") or prof_fl["kernels"].get("k_far<false>")
+        roof_near = {"bound": "fp64", "kernels": "near + self stages (" + ", ".join(prof_fl["near_stage_kernels"]) + ")",
+                     "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "flop_per_step": nf, "stage_ms": pair_ms,
+                     "flop_source": "ncu SASS dfma/dadd/dmul counts, profiles/r01_fp64_flops_config2.json",
+                     "per_kernel_frac_ncu": {k: round(v["fp64_flops"] / (v["ncu_ms"] * 1e-3) / 1e12 / peak, 3)
+                                             for k, v in prof_fl["kernels"].items()
+                                             if k in prof_fl["near_stage_kernels"] and v["fp64_flops"] > 1e9}}
+    else:
+        kf = None
+
     if rank == 0:
         s0 = stats[-1]
         list_ms = float(np.mean([s["t_list_ms"] for s in stats]))
@@ -371,6 +412,8 @@ def main():
                          "far": far_ms,
                          "near": float(np.mean([s["t_near_ms"] for s in stats])),
                          "self": float(np.mean([s["t_self_ms"] for s in stats]))},
+            # slowest step's stages (host round trips inside a stage show up here)
+            "split_ms_max": {k: float(max(s[f"t_{k}_ms"] for s in stats)) for k in ("list", "far", "near", "self")},
             "roofline": {"bound": "fp64", "kernel": "k_far (K2 direct far sum)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "peak_source": peak_src,
@@ -378,8 +421,10 @@ def main():
                          "pairs_per_s": T * S / (far_ms * 1e-3),
                          "survey_flop_per_pair": SURVEY_FAR_FLOP_PER_PAIR,
                          "survey_equiv_tflops": SURVEY_FAR_FLOP_PER_PAIR * T * S / (far_ms * 1e-3) / 1e12,
+                         "flop_per_pair_ncu": (kf["fp64_flops"] / (T * S)) if kf else None,
                          "traffic": prof.get("dram_bytes_per_launch"),
                          "traffic_source": prof.get("source")},
+            "roofline_near": roof_near,
             "far_method": args.far,
             "alt_far_method": alt,
             "gpu_launches": int(sum(s["gpu_launches"] for s in stats)),

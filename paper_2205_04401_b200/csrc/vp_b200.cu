@@ -283,6 +283,26 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 #ifndef VP_FAR_UNROLL
 #define VP_FAR_UNROLL 2
 #endif
+// K2's own log table: 2^VP_FAR_LOG_BITS entries replicated VP_FAR_COPIES
+// times (lane & (copies - 1) picks the copy).  With 11 index bits |t| <=
+// 2^-12 and a degree-3 minimax polynomial t + c2 t^2 + c3 t^3 is exact to
+// 1.9e-16 (absolute, log(1+t)), one DFMA fewer per pair than the 9-bit
+// table's degree-4 polynomial shared by the other kernels.
+#ifndef VP_FAR_LOG_BITS
+#define VP_FAR_LOG_BITS 10
+#endif
+#ifndef VP_FAR_COPIES
+#define VP_FAR_COPIES 8
+#endif
+// a table above 64 KB leaves room for one block per SM: 512 threads, so the
+// SM still holds 16 warps
+#if (1 << VP_FAR_LOG_BITS) * VP_FAR_COPIES * 16 > 65536
+#undef VP_FAR_MINB
+#define VP_FAR_MINB 1
+#ifndef VP_FAR_THREADS
+#define VP_FAR_THREADS 512
+#endif
+#endif
 #ifndef VP_FAR_THREADS
 #define VP_FAR_THREADS 256
 #endif
@@ -290,8 +310,49 @@ constexpr int FAR_THREADS = VP_FAR_THREADS;
 constexpr int FAR_R = VP_FAR_R;      // targets per thread (register tile)
 constexpr int FAR_TILE = 256;        // sources per shared-memory tile
 constexpr int kFarUnroll = VP_FAR_UNROLL;
+constexpr int kFarLogBits = VP_FAR_LOG_BITS;
+constexpr int kFarLogEntries = 1 << kFarLogBits;
+constexpr int kFarCopies = VP_FAR_COPIES;
+static_assert(kFarLogBits >= 9 && kFarLogBits <= 11, "far log table: 9..11 index bits");
+static_assert(kFarCopies == 2 || kFarCopies == 4 || kFarCopies == 8, "far log table copies");
 
-__device__ double2 g_logtab[kLogEntries];  // {r_k, -log r_k}, filled at vp_create
+__device__ double2 g_logtab[kLogEntries];      // {r_k, -log r_k}, filled at vp_create
+__device__ double2 g_fartab[kFarLogEntries];   // the same for K2's table
+
+// log r^2 for K2 (see far_log_r2 in vp_device.cuh for the bit manipulation)
+template <bool ZERO_CHECK>
+__device__ __forceinline__ double far_log_k2(const double2* tab, unsigned laneoff, unsigned c3ff, double x) {
+  if constexpr (kFarLogBits == 9 && kFarCopies == kLogCopies) {
+    return far_log_r2<ZERO_CHECK>(tab, laneoff, c3ff, x);
+  } else {
+    const unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+    unsigned off, mhi;
+    constexpr int kStrideLog = kFarCopies == 8 ? 7 : kFarCopies == 4 ? 6 : 5;  // entry stride 16 * copies
+    constexpr unsigned kShift = 20 - kFarLogBits - kStrideLog;
+    constexpr unsigned kMask = (unsigned)(kFarLogEntries - 1) << kStrideLog;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(off) : "r"(hi >> kShift), "n"(kMask), "r"(laneoff));
+    asm("lop3.b32 %0, %1, 0x000fffff, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(c3ff));
+    const double2 tb = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + off);
+    const double m = __hiloint2double((int)mhi, (int)lo);
+    const double ed = log_exponent(hi);
+    const double t = fma(m, tb.x, -1.0);
+    double p;
+    if constexpr (kFarLogBits == 11) {  // minimax on |t| <= 2^-12 (1.002x): 1.9e-16
+      double i = fma(t, 0.33333334272003357, -0.5000000117277289);
+      i = fma(t, i, 1.0);
+      p = fma(t, i, tb.y);
+    } else if constexpr (kFarLogBits == 10) {  // minimax on |t| <= 2^-11: 3.6e-15
+      double i = fma(t, 0.33333338120707445, -0.5000000598513419);
+      i = fma(t, i, 1.0);
+      p = fma(t, i, tb.y);
+    } else {
+      p = log1p_poly<false>(t, tb.y);
+    }
+    const double lg = fma(ed, 0.69314718055994530942, p);
+    if constexpr (ZERO_CHECK) return hi >= 0x00100000u ? lg : 0.0;
+    return lg;
+  }
+}
 
 template <bool ZERO_CHECK>
 __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
@@ -299,11 +360,11 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
           const double* __restrict__ sy, const double* __restrict__ sq, int64_t chunk,
           double* __restrict__ part, unsigned c3ff) {
   extern __shared__ __align__(16) unsigned char fsm[];
-  double2* tab = reinterpret_cast<double2*>(fsm);  // kLogEntries x kLogCopies
-  double2* sxy = tab + kLogEntries * kLogCopies;
+  double2* tab = reinterpret_cast<double2*>(fsm);  // kFarLogEntries x kFarCopies
+  double2* sxy = tab + kFarLogEntries * kFarCopies;
   double* ssq = reinterpret_cast<double*>(sxy + FAR_TILE);
-  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += FAR_THREADS) tab[i] = g_logtab[i / kLogCopies];
-  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  for (int i = threadIdx.x; i < kFarLogEntries * kFarCopies; i += FAR_THREADS) tab[i] = g_fartab[i / kFarCopies];
+  const unsigned laneoff = 16u * (threadIdx.x & (kFarCopies - 1));
   const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
   double tx[FAR_R], ty[FAR_R], acc[FAR_R];
 #pragma unroll
@@ -332,7 +393,7 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
       for (int r = 0; r < FAR_R; ++r) {
         const double dx = tx[r] - ps.x, dy = ty[r] - ps.y;
         const double r2 = fma(dx, dx, dy * dy);
-        acc[r] = fma(q, far_log_r2<ZERO_CHECK>(tab, laneoff, c3ff, r2), acc[r]);
+        acc[r] = fma(q, far_log_k2<ZERO_CHECK>(tab, laneoff, c3ff, r2), acc[r]);
       }
     }
   }
@@ -973,6 +1034,119 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
               const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
               acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
             }
+          }
+        }
+      }
+    }
+    const double val = warp_sum(acc);
+    if (lane == 0) part_t[t] = val;
+  }
+}
+
+// K4b cached leaves, evaluation form with leaf GROUPS: the warp takes G leaves
+// at a time and spreads their G * len_n rule nodes over its 32 * S lane slots
+// (slot s = lane + 32 k -> leaf s / len_n, node s % len_n, fixed per lane).
+// For the N_n = 12 near rule (49 nodes) G = 3, S = 5 fills 147 of 160 slots
+// (92 %; the one-leaf layout of k_near_ct fills 49 of 64) and gives each lane
+// S independent log chains per step instead of 2.  Per slot the lane reads
+// its leaf's D0/BA/CA (two leaves per instruction at most: distinct 32-B
+// rows, no bank conflict) and the cache value G of (leaf, node); the next
+// group's G values are loaded while the current group computes.  Slots of a
+// leaf past the batch end (and the S * 32 - G * len_n spare slots) weigh 0;
+// their geometry is finite (zeroed / a previous batch's), so 0 * log stays 0.
+// Summation order per target is fixed (group, slot), independent of the
+// launch shape.
+constexpr int NG_WARPS = 8;
+template <int S>
+__global__ void __launch_bounds__(NG_WARPS * 32, 2)
+    k_near_cg(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
+              const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
+              const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
+              const double* __restrict__ gcache, const double* __restrict__ slot_ref, int cache_depth, int G,
+              double* __restrict__ part_t, unsigned c3ff) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
+  constexpr int kRows = 32 + 4;                    // a batch + G - 1 <= 3 spare rows
+  __shared__ double4 sD[NG_WARPS][kRows];
+  __shared__ double2 sC[NG_WARPS][kRows];
+  __shared__ long long sgo[NG_WARPS][kRows];
+  const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
+  for (int i = threadIdx.x; i < NG_WARPS * kRows; i += blockDim.x) {
+    (&sD[0][0])[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+    (&sC[0][0])[i] = make_double2(0.0, 0.0);
+    (&sgo[0][0])[i] = 0;
+  }
+  const int Ln = R->len_n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nu[S], nv[S];
+  int lgk[S], ndk[S];  // leaf within the group (-1: spare slot), rule node
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int s = lane + 32 * k;
+    const int lg = s / Ln;
+    const bool ok = lg < G;
+    lgk[k] = ok ? lg : -1;
+    ndk[k] = ok ? s - lg * Ln : 0;
+    nu[k] = ok ? R->near_x[ndk[k]] : 0.0;
+    nv[k] = ok ? R->near_y[ndk[k]] : 0.0;
+  }
+  __syncthreads();
+  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
+    const int64_t q0 = toff[t], q1 = toff[t + 1];
+    double acc = 0.0;
+    if (q1 > q0) {
+      const int64_t L0 = loff[q0], L1 = loff[q1];
+      const double2 tp = txy[t];
+      const double tx = tp.x, ty = tp.y;
+      int64_t q = q0;  // this lane's current pair (leaves ascend with the lane's batches)
+      for (int64_t lb = L0; lb < L1; lb += 32) {
+        const int nb = (int)min((int64_t)32, L1 - lb);
+        __syncwarp();
+        if (lane < nb) {
+          const int64_t Lf = lb + lane;
+          while (loff[q + 1] <= Lf) ++q;
+          const int32_t e = pair_elem[q];
+          const unsigned long long code = leaves[Lf];
+          const int d = (int)(code >> 58);
+          const ElemRec& Er = el[e];
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const double* r = slot_ref + 6 * slot;
+          const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
+          const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
+          sD[wid][lane] = make_double4(tx - pax, ty - pay, fma(r[3], Er.e2x, r[2] * Er.e1x),
+                                       fma(r[3], Er.e2y, r[2] * Er.e1y));
+          sC[wid][lane] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
+          sgo[wid][lane] = ((long long)e * nslot + slot) * Ln;
+        }
+        __syncwarp();
+        double gn[S];
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          const int l = lgk[k];
+          gn[k] = (l >= 0 && l < nb) ? __ldg(gcache + sgo[wid][l] + ndk[k]) : 0.0;
+        }
+#pragma unroll 1
+        for (int li = 0; li < nb; li += G) {
+          double g[S];
+#pragma unroll
+          for (int k = 0; k < S; ++k) g[k] = gn[k];
+          if (li + G < nb) {
+#pragma unroll
+            for (int k = 0; k < S; ++k) {
+              const int l = li + G + lgk[k];
+              gn[k] = (lgk[k] >= 0 && l < nb) ? __ldg(gcache + sgo[wid][l] + ndk[k]) : 0.0;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < S; ++k) {
+            const int l = li + max(lgk[k], 0);
+            const double4 dd = sD[wid][l];
+            const double2 cc = sC[wid][l];
+            const double dx = fma(-nu[k], dd.z, fma(-nv[k], cc.x, dd.x));
+            const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
+            acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
           }
         }
       }
@@ -1849,6 +2023,7 @@ struct vp_ctx {
   DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
   DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
+  int64_t free_mem_at_first_near = -1;
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
@@ -2099,6 +2274,31 @@ void launch_near_ct(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pe
       0x3ff00000u);
 }
 
+// Leaf-group shape of k_near_cg: G leaves over 32*S lane slots, the G in 1..4
+// (S <= 5) with the highest slot utilisation G*len_n / (32*S); 0 if len_n > 160.
+inline int near_group_shape(int Ln, int* S_out) {
+  int bestG = 0, bestS = 0;
+  double best = 0.0;
+  for (int G = 1; G <= 4; ++G) {
+    const int S = (G * Ln + 31) / 32;
+    if (S > 5) break;
+    const double u = (double)(G * Ln) / (32.0 * S);
+    if (u > best + 1e-12) best = u, bestG = G, bestS = S;
+  }
+  *S_out = bestS;
+  return bestG;
+}
+
+template <int S>
+void launch_near_cg(vp_ctx* c, int G, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
+                    const double* gc) {
+  const int blocks = (int)std::min<int64_t>(nblk(T, NG_WARPS), (int64_t)c->sm_count * 24);
+  k_near_cg<S><<<std::max(blocks, 1), NG_WARPS * 32, sizeof(LogTab), c->stream>>>(
+      T, toff, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
+      c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, G, c->d_neart.as<double>(),
+      0x3ff00000u);
+}
+
 #define VP_DISPATCH_K(k, F, ...)     \
   switch (k) {                       \
     case 1: F<1>(__VA_ARGS__); break; \
@@ -2123,7 +2323,20 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
                                c->d_sq.as<double>(), c->d_nps.as<double>(), true);
   if (c->cache_depth >= 0 && toff) {  // evaluation: per-target sums of the cached leaves
     cudaMemsetAsync(c->d_npa.p, 0, sizeof(double) * n, c->stream);
-    VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_ct, c, T, toff, pelem, txy, gc);
+    int S = 0;
+    const int G = near_group_shape(c->rules.len_n, &S);
+    static const bool force_ct = getenv("VP_NEAR_CT") != nullptr;  // A/B switch: one-leaf layout
+    if (G > 0 && !force_ct) {
+      switch (S) {
+        case 1: launch_near_cg<1>(c, G, T, toff, pelem, txy, gc); break;
+        case 2: launch_near_cg<2>(c, G, T, toff, pelem, txy, gc); break;
+        case 3: launch_near_cg<3>(c, G, T, toff, pelem, txy, gc); break;
+        case 4: launch_near_cg<4>(c, G, T, toff, pelem, txy, gc); break;
+        default: launch_near_cg<5>(c, G, T, toff, pelem, txy, gc); break;
+      }
+    } else {
+      VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_ct, c, T, toff, pelem, txy, gc);
+    }
   } else if (c->cache_depth >= 0) {
     VP_DISPATCH_K((c->rules.len_n + 31) / 32, launch_near_c, c, cblocks, n, ptgt, pelem, txy, gc);
   } else {
@@ -2167,9 +2380,13 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_ldeep.ensure(sizeof(int32_t) * (n + 1)));
   // scratch for the first `cap` leaves of every pair, within a memory budget:
   // the larger of leaf_scratch_budget and 10 % of the free device memory
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
-  const int64_t budget = std::max<int64_t>(c->leaf_scratch_budget, (int64_t)(free_b / 10));
+  // (free memory is sampled once per context: no driver query per evaluation)
+  if (c->free_mem_at_first_near < 0) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    c->free_mem_at_first_near = (int64_t)free_b;
+  }
+  const int64_t budget = std::max<int64_t>(c->leaf_scratch_budget, c->free_mem_at_first_near / 10);
   const int cap = (int)std::min<int64_t>(64, (budget / 8) / std::max<int64_t>(n, 1));
   CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
@@ -2422,7 +2639,7 @@ int compute_sources(vp_ctx* c) {
   return 0;
 }
 
-constexpr size_t kFarSmem = sizeof(LogTab) + FAR_TILE * (sizeof(double2) + sizeof(double));
+constexpr size_t kFarSmem = sizeof(double2) * kFarLogEntries * kFarCopies + FAR_TILE * (sizeof(double2) + sizeof(double));
 
 int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check, DevBuf& part);
 int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check);
@@ -2792,6 +3009,11 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_near_ct<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_ct<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cg<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cg<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
@@ -2802,12 +3024,15 @@ int vp_create(int device, vp_ctx** out) {
   }
   double2 lt[kLogEntries];
   log_table_fill(lt);
+  static double2 ltf[kFarLogEntries];
+  log_table_fill(ltf, kFarLogEntries);
   double la[kMaxCurveDeg + 1], lb[kMaxCurveDeg + 1];
   for (int k = 0; k <= kMaxCurveDeg; ++k) {
     la[k] = leg_la(k);
     lb[k] = leg_lb(k);
   }
   if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_fartab, ltf, sizeof(ltf)) != cudaSuccess ||
       cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess ||
       cudaMemcpyToSymbol(c_leg_la, la, sizeof(la)) != cudaSuccess ||
       cudaMemcpyToSymbol(c_leg_lb, lb, sizeof(lb)) != cudaSuccess) {

@@ -235,9 +235,9 @@ struct LogTab {
   double2 e[kLogEntries * kLogCopies];  // entry k, copy c at k*8 + c
 };
 
-inline void log_table_fill(double2* host /* kLogEntries */) {
-  for (int k = 0; k < kLogEntries; ++k) {
-    const long double mk = 1.0L + ((long double)k + 0.5L) / (long double)kLogEntries;
+inline void log_table_fill(double2* host /* n */, int n = kLogEntries) {
+  for (int k = 0; k < n; ++k) {
+    const long double mk = 1.0L + ((long double)k + 0.5L) / (long double)n;
     const double r = (double)(1.0L / mk);
     host[k].x = r;
     host[k].y = (double)(-log1pl((long double)r - 1.0L));
