@@ -470,6 +470,31 @@ __device__ __forceinline__ void decode_path(unsigned long long path, int d, doub
   }
 }
 
+// decode_path in integer arithmetic: the reference vertices of a depth-d
+// sub-simplex are dyadic, (i, j) * 2^-d with 0 <= i, j <= 2^d; midpoints at
+// scale 2^-l are sums at scale 2^-(l+1).  The doubles built from them are the
+// exact values decode_path computes (its halvings are exact), for a few
+// integer adds per level instead of 12 FP64 operations.
+__device__ __forceinline__ void decode_path_i(unsigned long long path, int d, double& ax, double& ay,
+                                              double& bx, double& by, double& cx, double& cy) {
+  int aX = 0, aY = 0, bX = 1, bY = 0, cX = 0, cY = 1;
+  for (int l = d - 1; l >= 0; --l) {
+    const int ch = (int)((path >> (2 * l)) & 3ull);
+    const int abX = aX + bX, abY = aY + bY, bcX = bX + cX, bcY = bY + cY, caX = cX + aX, caY = cY + aY;
+    const int AX = aX << 1, AY = aY << 1, BX = bX << 1, BY = bY << 1, CX = cX << 1, CY = cY << 1;
+    aX = ch == 0 ? AX : ch == 1 ? abX : ch == 2 ? caX : bcX;
+    aY = ch == 0 ? AY : ch == 1 ? abY : ch == 2 ? caY : bcY;
+    bX = ch == 0 ? abX : ch == 1 ? BX : ch == 2 ? bcX : caX;
+    bY = ch == 0 ? abY : ch == 1 ? BY : ch == 2 ? bcY : caY;
+    cX = ch == 0 ? caX : ch == 1 ? bcX : ch == 2 ? CX : abX;
+    cY = ch == 0 ? caY : ch == 1 ? bcY : ch == 2 ? CY : abY;
+  }
+  const double s = ldexp(1.0, -d);
+  ax = (double)aX * s; ay = (double)aY * s;
+  bx = (double)bX * s; by = (double)bY * s;
+  cx = (double)cX * s; cy = (double)cY * s;
+}
+
 // acceptance test of one sub-simplex (same operation order as the oracle's
 // near_rec): rho_d = rho0n 4^{-d/N_n}; rho_d <= 1 accepts.
 constexpr int kBallMaxDepth = 20;  // ball model: accept at this depth (oracle: same)
@@ -555,6 +580,14 @@ struct LeafOut {
   int D;
 };
 
+// Load balance: leaf counts per pair vary from 1 to hundreds, so a thread
+// per pair leaves most lanes of a warp idle behind its largest pair.  Each
+// warp instead owns a chunk of `chunk` pairs (kLeafChunk; 32 = one pair per
+// lane for the few overflow pairs of the fill pass); a lane walks one pair at a
+// time (its own DFS, so a pair's leaves keep the oracle's order), and lanes
+// whose pair is done take the chunk's next pair (ballot + prefix count: the
+// assignment is warp-synchronous, and a pair's outputs do not depend on it).
+constexpr int kLeafChunk = 128;
 template <bool FILL>
 __global__ void __launch_bounds__(128)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
@@ -563,69 +596,99 @@ __global__ void __launch_bounds__(128)
                   int64_t* __restrict__ cnt, LeafOut lo, unsigned long long* __restrict__ stats,
                   int* __restrict__ err, CurvesDev CV, const int32_t* __restrict__ plist,
                   unsigned long long* __restrict__ scratch, int cap, int32_t* __restrict__ over,
-                  unsigned* __restrict__ n_over) {
+                  unsigned* __restrict__ n_over, int chunk) {
   __shared__ double skd[kMaxNearDepth + 2];
   for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
   const double ball_factor = R->near_model == 1 ? R->ball_factor : 0.0;
-  const int64_t pi_ = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t p = plist ? (pi_ < n_pairs ? plist[pi_] : INT64_MAX) : pi_;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t c0 = wg * chunk, c1 = min(n_pairs, c0 + chunk);
   unsigned long long rle1 = 0;
   int maxd = 0;
-  if (pi_ < n_pairs && curve_id_of(CV, pair_elem[p]) >= 0) {
-    if (!FILL) cnt[p] = lo.cntc[p] = lo.cntd[p] = 0;  // curved element: k_near_curved
-  } else if (pi_ < n_pairs) {
-    const int32_t e = pair_elem[p];
-    const double2 tp = txy[pair_tgt[p]];
-    const ElemRec E = el[e];
-    double l0[3];
-    side_lengths0(E, l0);
-    int gd = -1;
-    double gv = 0.0;
-    unsigned long long stack[kStackCap];
-    int sp = 0;
-    stack[sp++] = 0ull;
-    int64_t n = 0, nc = 0, oc = FILL ? lo.offc[p] : 0, od = FILL ? lo.offd[p] : 0;
-    bool bad = false;
-    while (sp > 0) {
-      const unsigned long long code = stack[--sp];
-      const int d = (int)(code >> 58);
-      const unsigned long long path = code & kPathMask;
-      double ax, ay, bx, by, cx, cy;
-      decode_path(path, d, ax, ay, bx, by, cx, cy);
-      bool le1;
-      if (near_accept(E, tp.x, tp.y, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd,
-                      gv)) {
-        if (FILL) {
-          if (d <= lo.D) lo.leafc[oc++] = code;
-          else lo.leafd[od++] = code;
-        } else if (n < cap) {
-          scratch[p * cap + n] = code;
+  int64_t cursor = c0;  // warp-uniform: next unassigned pair of the chunk
+  bool act = false;
+  int64_t p = 0;
+  double tx = 0.0, ty = 0.0;
+  ElemRec E;
+  double l0[3];
+  int gd = -1;
+  double gv = 0.0;
+  unsigned long long stack[kStackCap];
+  int sp = 0;
+  int64_t n = 0, nc = 0, oc = 0, od = 0;
+  while (true) {
+    const unsigned wm = __ballot_sync(0xffffffffu, !act);
+    if (wm) {
+      const int64_t mine = cursor + __popc(wm & lt_mask);
+      cursor += __popc(wm);
+      if (!act && mine < c1) {
+        p = plist ? plist[mine] : mine;
+        if (curve_id_of(CV, pair_elem[p]) >= 0) {
+          if (!FILL) cnt[p] = lo.cntc[p] = lo.cntd[p] = 0;  // curved element: k_near_curved
+        } else {
+          const double2 tp = txy[pair_tgt[p]];
+          tx = tp.x;
+          ty = tp.y;
+          E = el[pair_elem[p]];
+          side_lengths0(E, l0);
+          gd = -1;
+          sp = 0;
+          stack[sp++] = 0ull;
+          n = nc = 0;
+          if (FILL) {
+            oc = lo.offc[p];
+            od = lo.offd[p];
+          }
+          act = true;
         }
-        ++n;
-        nc += d <= lo.D ? 1 : 0;
-        rle1 += le1 ? 1ull : 0ull;
-        maxd = max(maxd, d);
-      } else {
-        if (d + 1 > kMaxPathDepth || sp + 4 > kStackCap) {
-          bad = true;
-          break;
-        }
-        const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
-        stack[sp++] = base | 3ull;
-        stack[sp++] = base | 2ull;
-        stack[sp++] = base | 1ull;
-        stack[sp++] = base;
       }
     }
-    if (bad) atomicExch(err, 2);
-    if (!FILL) {
-      if (bad) n = nc = 0;
-      cnt[p] = n;
-      lo.cntc[p] = nc;
-      lo.cntd[p] = n - nc;
-      if (n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)p;
-      if (n > nc) lo.deep[atomicAdd(lo.n_deep, 1u)] = (int32_t)p;
+    if (!__any_sync(0xffffffffu, act)) {
+      if (cursor >= c1) break;
+      continue;
+    }
+    if (!act) continue;
+    // one node of this lane's pair
+    const unsigned long long code = stack[--sp];
+    const int d = (int)(code >> 58);
+    const unsigned long long path = code & kPathMask;
+    double ax, ay, bx, by, cx, cy;
+    decode_path_i(path, d, ax, ay, bx, by, cx, cy);
+    bool le1;
+    bool bad = false;
+    if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd, gv)) {
+      if (FILL) {
+        if (d <= lo.D) lo.leafc[oc++] = code;
+        else lo.leafd[od++] = code;
+      } else if (n < cap) {
+        scratch[p * cap + n] = code;
+      }
+      ++n;
+      nc += d <= lo.D ? 1 : 0;
+      rle1 += le1 ? 1ull : 0ull;
+      maxd = max(maxd, d);
+    } else if (d + 1 > kMaxPathDepth || sp + 4 > kStackCap) {
+      bad = true;
+    } else {
+      const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
+      stack[sp++] = base | 3ull;
+      stack[sp++] = base | 2ull;
+      stack[sp++] = base | 1ull;
+      stack[sp++] = base;
+    }
+    if (bad || sp == 0) {  // the pair is done
+      if (bad) atomicExch(err, 2);
+      if (!FILL) {
+        if (bad) n = nc = 0;
+        cnt[p] = n;
+        lo.cntc[p] = nc;
+        lo.cntd[p] = n - nc;
+        if (n > cap) over[atomicAdd(n_over, 1u)] = (int32_t)p;
+        if (n > nc) lo.deep[atomicAdd(lo.n_deep, 1u)] = (int32_t)p;
+      }
+      act = false;
     }
   }
   if (!FILL) {
@@ -633,7 +696,7 @@ __global__ void __launch_bounds__(128)
       rle1 += __shfl_xor_sync(0xffffffffu, rle1, o);
       maxd = max(maxd, __shfl_xor_sync(0xffffffffu, maxd, o));
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       if (rle1) atomicAdd(&stats[1], rle1);
       atomicMax(&stats[2], (unsigned long long)maxd);
     }
@@ -2394,10 +2457,10 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, 2 * sizeof(unsigned), c->stream));
   LeafOut lo{c->d_lcntc.as<int64_t>(), c->d_lcntd.as<int64_t>(), c->d_loffc.as<int64_t>(), c->d_loffd.as<int64_t>(),
              nullptr, nullptr, c->d_ldeep.as<int32_t>(), c->d_nover.as<unsigned>() + 1, c->cache_depth};
-  k_near_leaves<false><<<nblk(n, 128), 128, 0, c->stream>>>(
+  k_near_leaves<false><<<nblk(n, 4 * kLeafChunk), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), lo,
       c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
-      c->d_lscratch.as<unsigned long long>(), cap, c->d_lover.as<int32_t>(), c->d_nover.as<unsigned>());
+      c->d_lscratch.as<unsigned long long>(), cap, c->d_lover.as<int32_t>(), c->d_nover.as<unsigned>(), kLeafChunk);
   CUDA_TRY(c, cudaMemsetAsync(c->d_lcntc.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->d_lcntd.as<int64_t>() + n, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
@@ -2427,7 +2490,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
     k_near_leaves<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
         nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, lo,
         c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0,
-        nullptr, nullptr);
+        nullptr, nullptr, 32);
   if (int rc = build_near_cache(c)) return rc;
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
