@@ -1111,51 +1111,61 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
 // (slot s = lane + 32 k -> leaf s / len_n, node s % len_n, fixed per lane).
 // For the N_n = 12 near rule (49 nodes) G = 3, S = 5 fills 147 of 160 slots
 // (92 %; the one-leaf layout of k_near_ct fills 49 of 64) and gives each lane
-// S independent log chains per step instead of 2.  Per slot the lane reads
-// its leaf's D0/BA/CA (two leaves per instruction at most: distinct 32-B
-// rows, no bank conflict) and the cache value G of (leaf, node); the next
-// group's G values are loaded while the current group computes.  Slots of a
-// leaf past the batch end (and the S * 32 - G * len_n spare slots) weigh 0;
-// their geometry is finite (zeroed / a previous batch's), so 0 * log stays 0.
-// Summation order per target is fixed (group, slot), independent of the
-// launch shape.
+// S independent log chains per step instead of 2.  A leaf is a row of four
+// 16-B fields in shared memory -- D0 = t - P_a, BA, CA and the address of
+// its cache row -- stored field-major (row stride 16 B: the batch's writes
+// and the reads of adjacent rows are bank-conflict free), so a slot costs one
+// address add, four shared loads at immediate offsets and one global load of
+// G (loaded a group ahead) besides its 12 FP64 operations.  Rows past the
+// batch end are zero geometry with the address of a zero row, so they add
+// exactly 0 without a test; the S*32 - G*len_n spare slots (all in slot
+// S - 1) are masked.  Summation order per target is fixed (group, slot).
 constexpr int NG_WARPS = 8;
+constexpr int kLeafRows = 32 + 4;  // a batch + G - 1 <= 3 zero rows
+struct LeafRows {
+  double2 d0[NG_WARPS][kLeafRows];
+  double2 ba[NG_WARPS][kLeafRows];
+  double2 ca[NG_WARPS][kLeafRows];
+  ulonglong2 g[NG_WARPS][kLeafRows];  // .x: address of the leaf's cache row
+};
+constexpr int kOffBA = (int)sizeof(double2) * NG_WARPS * kLeafRows;  // field offsets from d0
+constexpr int kOffCA = 2 * kOffBA, kOffG = 3 * kOffBA;
 template <int S>
 __global__ void __launch_bounds__(NG_WARPS * 32, 2)
     k_near_cg(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
               const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
               const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
-              const double* __restrict__ gcache, const double* __restrict__ slot_ref, int cache_depth, int G,
-              double* __restrict__ part_t, unsigned c3ff) {
+              const double* __restrict__ gcache, const double* __restrict__ zrow,
+              const double* __restrict__ slot_ref, int cache_depth, int G, double* __restrict__ part_t,
+              unsigned c3ff) {
   extern __shared__ __align__(16) unsigned char nsm[];
   double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
-  constexpr int kRows = 32 + 4;                    // a batch + G - 1 <= 3 spare rows
-  __shared__ double4 sD[NG_WARPS][kRows];
-  __shared__ double2 sC[NG_WARPS][kRows];
-  __shared__ long long sgo[NG_WARPS][kRows];
+  __shared__ LeafRows sR;
   const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
   for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
-  for (int i = threadIdx.x; i < NG_WARPS * kRows; i += blockDim.x) {
-    (&sD[0][0])[i] = make_double4(0.0, 0.0, 0.0, 0.0);
-    (&sC[0][0])[i] = make_double2(0.0, 0.0);
-    (&sgo[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < NG_WARPS * kLeafRows; i += blockDim.x) {
+    (&sR.d0[0][0])[i] = (&sR.ba[0][0])[i] = (&sR.ca[0][0])[i] = make_double2(0.0, 0.0);
+    (&sR.g[0][0])[i] = make_ulonglong2((unsigned long long)zrow, 0ull);
   }
   const int Ln = R->len_n;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double nu[S], nv[S];
-  int lgk[S], ndk[S];  // leaf within the group (-1: spare slot), rule node
+  int roff[S], noff[S];  // byte offset of the slot's leaf row within a group, rule node
+  bool spare = false;    // slot S - 1 beyond the group's nodes
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int s = lane + 32 * k;
     const int lg = s / Ln;
     const bool ok = lg < G;
-    lgk[k] = ok ? lg : -1;
-    ndk[k] = ok ? s - lg * Ln : 0;
-    nu[k] = ok ? R->near_x[ndk[k]] : 0.0;
-    nv[k] = ok ? R->near_y[ndk[k]] : 0.0;
+    if (k == S - 1) spare = !ok;
+    roff[k] = ok ? lg * (int)sizeof(double2) : 0;
+    noff[k] = ok ? s - lg * Ln : 0;
+    nu[k] = ok ? R->near_x[noff[k]] : 0.0;
+    nv[k] = ok ? R->near_y[noff[k]] : 0.0;
   }
   __syncthreads();
   const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  const char* wrow = reinterpret_cast<const char*>(&sR.d0[wid][0]);
   for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
     const int64_t q0 = toff[t], q1 = toff[t + 1];
     double acc = 0.0;
@@ -1178,37 +1188,40 @@ __global__ void __launch_bounds__(NG_WARPS * 32, 2)
           const double* r = slot_ref + 6 * slot;
           const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
           const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
-          sD[wid][lane] = make_double4(tx - pax, ty - pay, fma(r[3], Er.e2x, r[2] * Er.e1x),
-                                       fma(r[3], Er.e2y, r[2] * Er.e1y));
-          sC[wid][lane] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
-          sgo[wid][lane] = ((long long)e * nslot + slot) * Ln;
+          sR.d0[wid][lane] = make_double2(tx - pax, ty - pay);
+          sR.ba[wid][lane] = make_double2(fma(r[3], Er.e2x, r[2] * Er.e1x), fma(r[3], Er.e2y, r[2] * Er.e1y));
+          sR.ca[wid][lane] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
+          sR.g[wid][lane] = make_ulonglong2((unsigned long long)(gcache + ((int64_t)e * nslot + slot) * Ln), 0ull);
+        } else if (lane < nb + 3) {  // zero rows after the batch (rows 32.. stay zero)
+          sR.d0[wid][lane] = sR.ba[wid][lane] = sR.ca[wid][lane] = make_double2(0.0, 0.0);
+          sR.g[wid][lane] = make_ulonglong2((unsigned long long)zrow, 0ull);
         }
         __syncwarp();
         double gn[S];
 #pragma unroll
-        for (int k = 0; k < S; ++k) {
-          const int l = lgk[k];
-          gn[k] = (l >= 0 && l < nb) ? __ldg(gcache + sgo[wid][l] + ndk[k]) : 0.0;
-        }
+        for (int k = 0; k < S; ++k)
+          gn[k] = __ldg(*reinterpret_cast<const double* const*>(wrow + roff[k] + kOffG) + noff[k]);
 #pragma unroll 1
         for (int li = 0; li < nb; li += G) {
           double g[S];
 #pragma unroll
           for (int k = 0; k < S; ++k) g[k] = gn[k];
+          if (spare) g[S - 1] = 0.0;
+          const char* grp = wrow + li * (int)sizeof(double2);
           if (li + G < nb) {
+            const char* nxt = grp + G * (int)sizeof(double2);
 #pragma unroll
-            for (int k = 0; k < S; ++k) {
-              const int l = li + G + lgk[k];
-              gn[k] = (lgk[k] >= 0 && l < nb) ? __ldg(gcache + sgo[wid][l] + ndk[k]) : 0.0;
-            }
+            for (int k = 0; k < S; ++k)
+              gn[k] = __ldg(*reinterpret_cast<const double* const*>(nxt + roff[k] + kOffG) + noff[k]);
           }
 #pragma unroll
           for (int k = 0; k < S; ++k) {
-            const int l = li + max(lgk[k], 0);
-            const double4 dd = sD[wid][l];
-            const double2 cc = sC[wid][l];
-            const double dx = fma(-nu[k], dd.z, fma(-nv[k], cc.x, dd.x));
-            const double dy = fma(-nu[k], dd.w, fma(-nv[k], cc.y, dd.y));
+            const char* r = grp + roff[k];
+            const double2 d0 = *reinterpret_cast<const double2*>(r);
+            const double2 ba = *reinterpret_cast<const double2*>(r + kOffBA);
+            const double2 ca = *reinterpret_cast<const double2*>(r + kOffCA);
+            const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
+            const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
             acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
           }
         }
@@ -2358,7 +2371,8 @@ void launch_near_cg(vp_ctx* c, int G, int64_t T, const int64_t* toff, const int3
   const int blocks = (int)std::min<int64_t>(nblk(T, NG_WARPS), (int64_t)c->sm_count * 24);
   k_near_cg<S><<<std::max(blocks, 1), NG_WARPS * 32, sizeof(LogTab), c->stream>>>(
       T, toff, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
-      c->d_rules.as<RulesDev>(), gc, c->d_slotref.as<double>(), c->cache_depth, G, c->d_neart.as<double>(),
+      c->d_rules.as<RulesDev>(), gc, gc + c->n_tri * (int64_t)(((1ll << (2 * (c->cache_depth + 1))) - 1) / 3) *
+      c->rules.len_n, c->d_slotref.as<double>(), c->cache_depth, G, c->d_neart.as<double>(),
       0x3ff00000u);
 }
 
@@ -2599,7 +2613,9 @@ int build_near_cache(vp_ctx* c) {
     c->cacheV_depth = D;
     c->cacheV_p = c->p;
   }
-  CUDA_TRY(c, c->d_gcache.ensure(sizeof(double) * (size_t)(c->n_tri * R)));
+  // + one zero row (k_near_cg's rows past a batch point there)
+  CUDA_TRY(c, c->d_gcache.ensure(sizeof(double) * (size_t)(c->n_tri * R + Ln + 64)));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_gcache.as<double>() + c->n_tri * R, 0, sizeof(double) * (Ln + 64), c->stream));
   if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
   dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
   k_near_cache<<<grid, 256, 0, c->stream>>>(c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(),
