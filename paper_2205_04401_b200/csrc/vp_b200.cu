@@ -750,6 +750,77 @@ __global__ void __launch_bounds__(256)
     if (k < ne) out[(e0 + k) * R + r] = acc[k];
 }
 
+// The same contraction on the FP64 tensor cores (north_star: DMMA for the
+// dense per-triangle coefficient-to-value contraction).  out = A . B with
+// A[e][j] = c_e,j |J_e| (E x M) and B = Vt (M x R): a block computes 32
+// elements x 64 rows; A and B tiles sit in shared memory with row strides
+// = 4 (mod 16) doubles so the m8n8k4 fragment loads are conflict-free; each
+// of the 4 warps owns 32 x 16 outputs (4 x 2 DMMA tiles, 16 accumulators).
+// K = M padded to a multiple of 4 with zeros.
+constexpr int kNcBM = 32, kNcBN = 64;
+__host__ __device__ constexpr int nc_stride(int k) { return k + ((4 - k % 16) + 16) % 16; }
+__global__ void __launch_bounds__(128)
+    k_near_cache_mma(int64_t E, int M, int64_t R, const double* __restrict__ Vt, const double* __restrict__ coeffs,
+                     const ElemRec* __restrict__ el, double* __restrict__ out) {
+  extern __shared__ __align__(16) double ncs[];
+  const int Kp = (M + 3) & ~3;
+  const int SA = nc_stride(Kp), SB = nc_stride(kNcBN);
+  double* As = ncs;                 // [kNcBM][SA]
+  double* Bs = ncs + kNcBM * SA;    // [Kp][SB]
+  const int64_t e0 = (int64_t)blockIdx.x * kNcBM;
+  const int64_t r0 = (int64_t)blockIdx.y * kNcBN;
+  __shared__ double sdet[kNcBM];
+  if (threadIdx.x < kNcBM) sdet[threadIdx.x] = e0 + threadIdx.x < E ? el[e0 + threadIdx.x].det : 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kNcBM * Kp; i += blockDim.x) {
+    const int m = i / Kp, j = i - m * Kp;
+    const int64_t e = e0 + m;
+    As[m * SA + j] = (e < E && j < M) ? coeffs[e * M + j] * sdet[m] : 0.0;  // |J_T| folded in
+  }
+  for (int i = threadIdx.x; i < Kp * kNcBN; i += blockDim.x) {
+    const int j = i / kNcBN, n = i - j * kNcBN;
+    const int64_t r = r0 + n;
+    Bs[j * SB + n] = (j < M && r < R) ? __ldg(Vt + (int64_t)j * R + r) : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  for (int k0 = 0; k0 < Kp; k0 += 4) {
+    double a[4], b[2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = As[(mi * 8 + g) * SA + k0 + t];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) b[ni] = Bs[(k0 + t) * SB + w * 16 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+            : "d"(a[mi]), "d"(b[ni]));
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int64_t e = e0 + mi * 8 + g;
+    if (e >= E) continue;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int64_t r = r0 + w * 16 + ni * 8 + 2 * t;
+      if (r < R) out[e * R + r] = acc[mi][ni][0];
+      if (r + 1 < R) out[e * R + r + 1] = acc[mi][ni][1];
+    }
+  }
+}
+inline size_t near_cache_mma_smem(int M) {
+  const int Kp = (M + 3) & ~3;
+  return sizeof(double) * ((size_t)kNcBM * nc_stride(Kp) + (size_t)Kp * nc_stride(kNcBN));
+}
+
 // NPT leaf nodes per call share the density coefficient loads
 template <int P, int NPT>
 __device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __restrict__ ltab,
@@ -2616,10 +2687,19 @@ int build_near_cache(vp_ctx* c) {
   // + one zero row (k_near_cg's rows past a batch point there)
   CUDA_TRY(c, c->d_gcache.ensure(sizeof(double) * (size_t)(c->n_tri * R + Ln + 64)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_gcache.as<double>() + c->n_tri * R, 0, sizeof(double) * (Ln + 64), c->stream));
-  if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
-  dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
-  k_near_cache<<<grid, 256, 0, c->stream>>>(c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(),
-                                            c->d_el.as<ElemRec>(), c->d_gcache.as<double>());
+  static const bool cache_simt = getenv("VP_NEAR_CACHE_SIMT") != nullptr;  // A/B switch: DFMA kernel
+  if (!cache_simt) {
+    if (nblk(R, kNcBN) > 65535u) return set_err(c, 1, "near cache: too many rows");
+    dim3 grid((unsigned)((c->n_tri + kNcBM - 1) / kNcBM), (unsigned)nblk(R, kNcBN));
+    k_near_cache_mma<<<grid, 128, near_cache_mma_smem(M), c->stream>>>(
+        c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(), c->d_el.as<ElemRec>(),
+        c->d_gcache.as<double>());
+  } else {
+    if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
+    dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
+    k_near_cache<<<grid, 256, 0, c->stream>>>(c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(),
+                                              c->d_el.as<ElemRec>(), c->d_gcache.as<double>());
+  }
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 1;
   return 0;
@@ -3093,6 +3173,7 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_near_cg<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cg<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cache_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)near_cache_mma_smem(kMaxModes)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||

@@ -409,3 +409,33 @@ def test_p12_on_config1_mesh():
         u_g, _ = ev.evaluate(sub)
     u_o, _, _ = O.evaluate(sub)
     assert rel(u_g, u_o) <= REL_TOL
+
+
+_VARIANT_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2205_04401_b200 as vp
+pr = vp.load_config(2)
+with vp.Evaluator(0) as ev:
+    ev.load(pr)
+    u, st = ev.evaluate(pr.txy[::7])
+np.save({out!r}, u)
+"""
+
+
+@pytest.mark.parametrize("env", [{"VP_NEAR_CT": "1"}, {"VP_NEAR_CACHE_SIMT": "1"}])
+def test_near_kernel_variants_agree(tmp_path, env):
+    """The one-leaf cached-leaf kernel (k_near_ct) and the DFMA near-cache
+    contraction (k_near_cache) -- the A/B alternatives of k_near_cg and the
+    DMMA k_near_cache_mma -- give the same u up to summation order."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k, e in enumerate([{}, env]):
+        out = str(tmp_path / f"u{k}.npy")
+        subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT.format(root=root, out=out)], check=True,
+                       env={**os.environ, **e}, timeout=600)
+        outs.append(np.load(out))
+    assert rel(outs[1], outs[0]) <= 1e-13

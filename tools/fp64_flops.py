@@ -5,7 +5,8 @@ counters (run on the GPU box):
 
 runs `ncu --metrics <duration, dfma/dadd/dmul thread counts>` over
 `bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-fmm` and writes, per
-kernel, the FP64 flops of one launch (2 per DFMA, 1 per DADD/DMUL; medians
+kernel, the FP64 flops of one launch (2 per DFMA, 1 per DADD/DMUL, the
+tensor-pipe FP64 ops of DMMA; medians
 over the run's launches -- every step does identical work) and its ncu
 duration.  bench.py turns the near-stage totals into the near-field
 roofline with its own live timing (the ncu durations are cold-cache and
@@ -21,9 +22,10 @@ import sys
 MET = {"gpu__time_duration.sum": "ns",
        "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum": "dfma",
        "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum": "dadd",
-       "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul"}
+       "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul",
+       "sm__ops_path_tensor_src_fp64.sum": "dmma"}  # DMMA flops (2 per FMA)
 # kernels of the near field (K4) and self (K5) stages of an evaluation
-NEAR_STAGE = ("k_near_leaves", "k_leaves_copy", "k_near_cache", "k_near_cg", "k_near_ct", "k_near_int",
+NEAR_STAGE = ("k_near_leaves", "k_leaves_copy", "k_near_cache", "k_near_cache_mma", "k_near_cg", "k_near_ct", "k_near_int",
               "k_psum_tgt", "k_self", "k_near_combine", "k_pair_tgt")
 
 
@@ -51,7 +53,7 @@ def main():
         per.setdefault(name, {}).setdefault(lid, {})[MET[met]] = val
     res = {}
     for name, launches in per.items():
-        fl = [2 * v.get("dfma", 0) + v.get("dadd", 0) + v.get("dmul", 0) for v in launches.values()]
+        fl = [2 * v.get("dfma", 0) + v.get("dadd", 0) + v.get("dmul", 0) + v.get("dmma", 0) for v in launches.values()]
         ns = [v.get("ns", 0) for v in launches.values()]
         res[name] = {"launches": len(fl), "fp64_flops": statistics.median(fl), "ncu_ms": statistics.median(ns) * 1e-6}
     near = {k: v for k, v in res.items() if k.split("<")[0] in NEAR_STAGE}
