@@ -1191,7 +1191,13 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
 // batch end are zero geometry with the address of a zero row, so they add
 // exactly 0 without a test; the S*32 - G*len_n spare slots (all in slot
 // S - 1) are masked.  Summation order per target is fixed (group, slot).
-constexpr int NG_WARPS = 8;
+#ifndef VP_NG_WARPS
+#define VP_NG_WARPS 8
+#endif
+#ifndef VP_NG_MINB
+#define VP_NG_MINB 2
+#endif
+constexpr int NG_WARPS = VP_NG_WARPS;
 constexpr int kLeafRows = 32 + 4;  // a batch + G - 1 <= 3 zero rows
 struct LeafRows {
   double2 d0[NG_WARPS][kLeafRows];
@@ -1202,7 +1208,7 @@ struct LeafRows {
 constexpr int kOffBA = (int)sizeof(double2) * NG_WARPS * kLeafRows;  // field offsets from d0
 constexpr int kOffCA = 2 * kOffBA, kOffG = 3 * kOffBA;
 template <int S>
-__global__ void __launch_bounds__(NG_WARPS * 32, 2)
+__global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
     k_near_cg(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
               const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
               const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
@@ -2171,6 +2177,7 @@ struct vp_ctx {
   DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
   int64_t free_mem_at_first_near = -1;
+  int tabs_p = -1;  // p of the density-independent tables (K1's V, near-cache Vt, SelfTab); -1: stale
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
@@ -3409,6 +3416,7 @@ int vp_set_rules(vp_ctx* c, const vp_rules* r) {
   c->have_rules = true;
   c->sources_valid = false;
   c->cacheV_depth = -2;
+  c->tabs_p = -1;
   if (c->have_mesh)
     if (int rc = build_elements(c)) return rc;
   if (int rc = upload_self_tab(c)) return rc;
@@ -3419,6 +3427,7 @@ int vp_set_rules(vp_ctx* c, const vp_rules* r) {
     CUDA_TRY(c, c->d_V.ensure(sizeof(double) * V.size()));
     CUDA_TRY(c, cudaMemcpyAsync(c->d_V.p, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->tabs_p = c->p;
   }
   return 0;
 }
@@ -3434,6 +3443,14 @@ int vp_set_density(vp_ctx* c, int p, const double* coeffs) {
   CUDA_TRY(c, cudaMemcpyAsync(c->d_coeffs.p, coeffs, sizeof(double) * c->n_tri * M, cudaMemcpyHostToDevice, c->stream));
   c->p = p;
   c->M = M;
+  c->have_density = true;
+  c->sources_valid = false;
+  // K1's Koornwinder table, the near-cache Vt and the SelfTab depend on (p,
+  // rules) only: a new density of the same order reuses them
+  if (c->have_rules && c->tabs_p == p) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return 0;
+  }
   if (c->have_rules) {
     const vp_rules& r = c->rules;
     std::vector<double> V((size_t)r.len_q * M);
@@ -3442,10 +3459,10 @@ int vp_set_density(vp_ctx* c, int p, const double* coeffs) {
     CUDA_TRY(c, cudaMemcpyAsync(c->d_V.p, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, c->stream));
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  c->have_density = true;
-  c->sources_valid = false;
   c->cacheV_depth = -2;
-  return upload_self_tab(c);
+  if (int rc = upload_self_tab(c)) return rc;
+  c->tabs_p = c->have_rules ? p : -1;
+  return 0;
 }
 
 int vp_build_nearlist(vp_ctx* c, int64_t n_tgt, const double* txy, int32_t* self_out, int64_t* offsets_out,
