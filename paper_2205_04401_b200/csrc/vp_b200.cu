@@ -1447,6 +1447,12 @@ struct SelfTab {
   // sigma-direction transform straight to monomials in x = 2 sigma - 1:
   // PM[j][b] = sum_k [x^j]P_k(x) PL[k][b] (p <= kSelfHornerMaxP: Horner at the nodes)
   double PM[(kMaxPdev + 1) * (kMaxPdev + 1)];
+  // f(y(r, sigma)) = F(r, s = r sigma) with F of total degree <= p in (r, s):
+  // M = (p+1)(p+2)/2 samples at Fekete-type points (sr, ss) of the triangle
+  // 0 <= s <= r <= 1 determine it, and the whole chain grid -> (PL, PM) ->
+  // moments is one linear map T2 [2(p+1) x M]: (Eb, Ec) = T2 f(samples).
+  double sr[kMaxModes], ss[kMaxModes];
+  double T2[2 * (kMaxPdev + 1) * kMaxModes];
 };
 
 template <int P>
@@ -1458,13 +1464,13 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
            const SelfTab* __restrict__ ST, double* __restrict__ corr, double* __restrict__ sub_out,
            int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV) {
   constexpr int M = (P + 1) * (P + 2) / 2;
-  constexpr int NP = P + 1, NP2 = NP * NP;
-  constexpr int SNPT = NP2 <= 32 ? 1 : (NP2 <= 64 ? 2 : 3);
+  constexpr int NP = P + 1;
+  constexpr int SNPT = M <= 32 ? 1 : (M <= 64 ? 2 : 3);
   __shared__ double scc[SELF_WARPS][M];
-  __shared__ double sV[SELF_WARPS][NP2], sW[SELF_WARPS][NP2], sE[SELF_WARPS][2 * NP];
+  __shared__ double sF[SELF_WARPS][M], sE[SELF_WARPS][2 * NP];
   __shared__ double sB[SELF_WARPS][kMaxSelfPanels + 1];
   constexpr bool kHorner = P <= kSelfHornerMaxP;
-  __shared__ double sPL[NP2], sPM[NP2], sgx[NP], sbt[NP], sct[NP], sla[NP], slb[NP];
+  __shared__ double sT2[2 * NP * M], ssr[M], sss[M], sla[NP], slb[NP];
   __shared__ double sglx[kMaxGL], sglw[kMaxGL];
   __shared__ double2 sltab[kLogEntries];
   for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
@@ -1473,22 +1479,19 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     sglx[i] = R->gl_x[i];
     sglw[i] = R->gl_w[i];
   }
-  for (int i = threadIdx.x; i < NP2; i += blockDim.x) {
-    sPL[i] = ST->PL[i];
-    sPM[i] = kHorner ? ST->PM[i] : ST->PL[i];
+  for (int i = threadIdx.x; i < 2 * NP * M; i += blockDim.x) sT2[i] = ST->T2[i];
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    ssr[i] = ST->sr[i];
+    sss[i] = ST->ss[i];
   }
   for (int i = threadIdx.x; i < NP; i += blockDim.x) {
-    sgx[i] = ST->gx[i];
-    sbt[i] = ST->bt[i];
-    sct[i] = ST->ct[i];
     sla[i] = ST->la[i];
     slb[i] = ST->lb[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* cc = scc[wid];
-  double* V = sV[wid];
-  double* W = sW[wid];
+  double* F = sF[wid];
   double* Eb = sE[wid];
   double* Ec = sE[wid] + NP;
   unsigned long long my_panels = 0, my_degen = 0;
@@ -1531,48 +1534,30 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
       const double BRx = (k == 0 ? 1.0 : 0.0) - Arx, BRy = (k == 1 ? 1.0 : 0.0) - Ary;
       const double avx = Arx - txi, avy = Ary - teta;  // A - v in reference coordinates
-      // (1) f on the (p+1)^2 Gauss-Legendre grid (r_a, sigma_b), SNPT points per
-      // lane and call (one round of the warp for p <= 8)
-      for (int i = SNPT * lane; i < NP2; i += 32 * SNPT) {
+      // (1) f at the M Fekete-type samples y = v + r (A - v) + s (B - A) of the
+      // sub-triangle (f has total degree <= p in (r, s)), SNPT per lane (one
+      // round of the warp for p <= 10)
+      for (int i = SNPT * lane; i < M; i += 32 * SNPT) {
         double xs[SNPT], ys[SNPT], f[SNPT];
 #pragma unroll
         for (int q = 0; q < SNPT; ++q) {
-          const int iq = min(i + q, NP2 - 1);
-          const int a = iq / NP, b = iq - a * NP;
-          xs[q] = fma(sgx[a], fma(sgx[b], BRx, avx), txi);
-          ys[q] = fma(sgx[a], fma(sgx[b], BRy, avy), teta);
+          const int iq = min(i + q, M - 1);
+          xs[q] = fma(sss[iq], BRx, fma(ssr[iq], avx, txi));
+          ys[q] = fma(sss[iq], BRy, fma(ssr[iq], avy, teta));
         }
         density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
 #pragma unroll
         for (int q = 0; q < SNPT; ++q)
-          if (i + q < NP2) V[i + q] = f[q];
+          if (i + q < M) F[i + q] = f[q];
       }
       __syncwarp();
-      // (2) Legendre coefficients in r: W[n][b] = sum_a PL[n][a] V[a][b]
-      for (int o = lane; o < NP2; o += 32) {
-        const int n = o / NP, bb = o - n * NP;
-        double sum = 0.0;
-#pragma unroll
-        for (int aa = 0; aa < NP; ++aa) sum = fma(sPL[n * NP + aa], V[aa * NP + bb], sum);
-        W[o] = sum;
-      }
-      __syncwarp();
-      // (3) and in sigma: A[n][kk] = sum_b PL[kk][b] W[n][b]   (into V)
-      for (int o = lane; o < NP2; o += 32) {
-        const int n = o / NP, kk = o - n * NP;
-        double sum = 0.0;
-#pragma unroll
-        for (int bb = 0; bb < NP; ++bb) sum = fma(sPM[kk * NP + bb], W[n * NP + bb], sum);
-        V[o] = sum;
-      }
-      __syncwarp();
-      // (4) contract the r direction with the GGQ-rule moments
+      // (2) the sigma polynomials of the GGQ-rule moments, (Eb, Ec) = T2 f
+      // (= Gauss-Legendre grid interpolation, Legendre transforms in r and
+      // sigma and the moment contraction, folded on the host)
       for (int o = lane; o < 2 * NP; o += 32) {
-        const int kk = o < NP ? o : o - NP;
-        const double* mom = o < NP ? sbt : sct;
         double sum = 0.0;
-#pragma unroll
-        for (int n = 0; n < NP; ++n) sum = fma(V[n * NP + kk], mom[n], sum);
+#pragma unroll 5
+        for (int q = 0; q < M; ++q) sum = fma(sT2[o * M + q], F[q], sum);
         sE[wid][o] = sum;
       }
       __syncwarp();
@@ -2712,6 +2697,125 @@ int build_near_cache(vp_ctx* c) {
   return 0;
 }
 
+// Sample set and map of the self kernel's density step (SelfTab::T2).
+// Points: approximate Fekete points of degree p on the reference triangle,
+// chosen by column-pivoted Gram-Schmidt on the orthonormal Koornwinder
+// basis over a 60 x 60 lattice (ties -> lowest index); Lebesgue constant
+// 2.7 / 4.8 / 11.2 / 17.3 at p = 4 / 6 / 8 / 12 (the shifted lattice of the
+// targets: 129 / 769 / 4097 / 98305).  (xi, eta) -> (r, s) = (1 - xi, eta).
+// T2 = Tgrid . R, where R [(p+1)^2 x M] interpolates the Gauss-Legendre grid
+// (r_a, r_a sigma_b) from the samples and Tgrid [2(p+1) x (p+1)^2] is the
+// PL / PM / moment chain of k_self; long double throughout.
+int self_sample_map(vp_ctx* c, SelfTab& T, const double* gx_m11) {
+  const int p = c->p, np = p + 1, M = koorn_size(p);
+  constexpr int G = 60;
+  std::vector<double> cx, cy;
+  for (int j = 0; j <= G; ++j)
+    for (int i = 0; i + j <= G; ++i) {
+      cx.push_back((double)i / G);
+      cy.push_back((double)j / G);
+    }
+  const int nc = (int)cx.size();
+  std::vector<long double> A((size_t)nc * M);
+  std::vector<double> kv(M);
+  for (int q = 0; q < nc; ++q) {
+    koorn_eval(p, cx[q], cy[q], kv.data());
+    for (int i = 0; i < M; ++i) A[(size_t)q * M + i] = kv[i];
+  }
+  std::vector<long double> nrm(nc);
+  std::vector<char> used(nc, 0);
+  std::vector<int> sel;
+  for (int q = 0; q < nc; ++q) {
+    long double v = 0.0L;
+    for (int i = 0; i < M; ++i) v += A[(size_t)q * M + i] * A[(size_t)q * M + i];
+    nrm[q] = v;
+  }
+  for (int k = 0; k < M; ++k) {
+    int best = -1;
+    for (int q = 0; q < nc; ++q)
+      if (!used[q] && (best < 0 || nrm[q] > nrm[best])) best = q;
+    if (best < 0 || !(nrm[best] > 0.0L)) return set_err(c, 2, "self table: sample selection failed");
+    used[best] = 1;
+    sel.push_back(best);
+    const long double inv = 1.0L / std::sqrt(nrm[best]);
+    std::vector<long double> qv(M);
+    for (int i = 0; i < M; ++i) qv[i] = A[(size_t)best * M + i] * inv;
+    for (int q = 0; q < nc; ++q) {
+      if (used[q]) continue;
+      long double d = 0.0L;
+      for (int i = 0; i < M; ++i) d += qv[i] * A[(size_t)q * M + i];
+      long double v = 0.0L;
+      for (int i = 0; i < M; ++i) {
+        A[(size_t)q * M + i] -= d * qv[i];
+        v += A[(size_t)q * M + i] * A[(size_t)q * M + i];
+      }
+      nrm[q] = v;
+    }
+  }
+  // B [M x M] = K_i at the samples (rows = samples); Binv by Gauss-Jordan
+  std::vector<long double> B((size_t)M * M), Bi((size_t)M * M, 0.0L);
+  for (int q = 0; q < M; ++q) {
+    koorn_eval(p, cx[sel[q]], cy[sel[q]], kv.data());
+    for (int i = 0; i < M; ++i) B[(size_t)q * M + i] = kv[i];
+    Bi[(size_t)q * M + q] = 1.0L;
+    T.sr[q] = 1.0 - cx[sel[q]];
+    T.ss[q] = cy[sel[q]];
+  }
+  for (int col = 0; col < M; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < M; ++r)
+      if (std::fabs(B[(size_t)r * M + col]) > std::fabs(B[(size_t)piv * M + col])) piv = r;
+    if (!(std::fabs(B[(size_t)piv * M + col]) > 0.0L)) return set_err(c, 2, "self table: singular sample matrix");
+    for (int k = 0; k < M; ++k) {
+      std::swap(B[(size_t)col * M + k], B[(size_t)piv * M + k]);
+      std::swap(Bi[(size_t)col * M + k], Bi[(size_t)piv * M + k]);
+    }
+    const long double d = 1.0L / B[(size_t)col * M + col];
+    for (int k = 0; k < M; ++k) {
+      B[(size_t)col * M + k] *= d;
+      Bi[(size_t)col * M + k] *= d;
+    }
+    for (int r = 0; r < M; ++r) {
+      if (r == col) continue;
+      const long double f = B[(size_t)r * M + col];
+      if (f == 0.0L) continue;
+      for (int k = 0; k < M; ++k) {
+        B[(size_t)r * M + k] -= f * B[(size_t)col * M + k];
+        Bi[(size_t)r * M + k] -= f * Bi[(size_t)col * M + k];
+      }
+    }
+  }
+  // (B^-1 maps sample values to Koornwinder coefficients: coef = Binv f since
+  // f_q = sum_i B[q][i] coef_i.)  R[(a,b)][q] = sum_i K_i(grid ab) Binv[i][q].
+  const bool horner = p <= kSelfHornerMaxP;
+  std::vector<long double> Tg((size_t)2 * np * np * np, 0.0L);  // [o][(a,b)]
+  for (int kk = 0; kk < np; ++kk)
+    for (int a = 0; a < np; ++a)
+      for (int b = 0; b < np; ++b) {
+        const long double pm = horner ? T.PM[kk * np + b] : T.PL[kk * np + b];
+        long double sb = 0.0L, sc = 0.0L;
+        for (int n = 0; n < np; ++n) {
+          sb += (long double)T.bt[n] * T.PL[n * np + a];
+          sc += (long double)T.ct[n] * T.PL[n * np + a];
+        }
+        Tg[(size_t)kk * np * np + a * np + b] = sb * pm;
+        Tg[(size_t)(np + kk) * np * np + a * np + b] = sc * pm;
+      }
+  std::vector<long double> T2((size_t)2 * np * M, 0.0L);
+  for (int a = 0; a < np; ++a)
+    for (int b = 0; b < np; ++b) {
+      const double r = 0.5 * (gx_m11[a] + 1.0), sg = 0.5 * (gx_m11[b] + 1.0);
+      koorn_eval(p, 1.0 - r, r * sg, kv.data());
+      for (int q = 0; q < M; ++q) {
+        long double rq = 0.0L;
+        for (int i = 0; i < M; ++i) rq += (long double)kv[i] * Bi[(size_t)i * M + q];
+        for (int o = 0; o < 2 * np; ++o) T2[(size_t)o * M + q] += Tg[(size_t)o * np * np + a * np + b] * rq;
+      }
+    }
+  for (size_t i = 0; i < T2.size(); ++i) T.T2[i] = (double)T2[i];
+  return 0;
+}
+
 // SelfTab for the current (p, GGQ rule): Gauss-Legendre interpolation grid
 // on [0,1], Legendre projection weights and the GGQ-rule moments.
 int upload_self_tab(vp_ctx* c) {
@@ -2767,6 +2871,7 @@ int upload_self_tab(vp_ctx* c) {
         T.PM[j * np + a] = (double)v;
       }
   }
+  if (int rc = self_sample_map(c, T, gx)) return rc;
   CUDA_TRY(c, c->d_selftab.ensure(sizeof(SelfTab)));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_selftab.p, &T, sizeof(SelfTab), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
