@@ -1455,6 +1455,15 @@ struct SelfTab {
   double T2[2 * (kMaxPdev + 1) * kMaxModes];
 };
 
+// Per target the warp handles the three sub-triangles together where their
+// work is independent: lanes 0-2 form the three side geometries, the
+// density samples of all three (3 M points) share one pass of the warp, and
+// the 3 x 2(p+1) moment polynomials one more; only the arc-length nodes
+// (dyadic panels x Gauss-Legendre) go side by side.
+struct SelfSide {
+  double Ax, Ay, ABx, ABy, L, h, st, avx, avy, BRx, BRy;
+  int N, Mr, npan, degenerate, pad;
+};
 template <int P>
 __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
@@ -1465,12 +1474,20 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
            int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV) {
   constexpr int M = (P + 1) * (P + 2) / 2;
   constexpr int NP = P + 1;
-  constexpr int SNPT = M <= 32 ? 1 : (M <= 64 ? 2 : 3);
+  constexpr int M3 = 3 * M;
+  // density samples per lane and pass over the 3 M points of a target
+#ifndef VP_SELF_SNPT_MAX
+#define VP_SELF_SNPT_MAX 5
+#endif
+  constexpr int SNPT0 = M3 <= 32 ? 1 : (M3 <= 64 ? 2 : (M3 <= 96 ? 3 : (M3 <= 128 ? 4 : 5)));
+  constexpr int SNPT = SNPT0 < VP_SELF_SNPT_MAX ? SNPT0 : VP_SELF_SNPT_MAX;
   __shared__ double scc[SELF_WARPS][M];
-  __shared__ double sF[SELF_WARPS][M], sE[SELF_WARPS][2 * NP];
+  __shared__ double sF[SELF_WARPS][M3], sE[SELF_WARPS][3][2 * NP];
   __shared__ double sB[SELF_WARPS][kMaxSelfPanels + 1];
+  __shared__ SelfSide sS[SELF_WARPS][3];
   constexpr bool kHorner = P <= kSelfHornerMaxP;
-  __shared__ double sT2[2 * NP * M], ssr[M], sss[M], sla[NP], slb[NP];
+  extern __shared__ __align__(16) double sT2[];  // [2 NP][M], dynamic
+  __shared__ double ssr[M], sss[M], sla[NP], slb[NP];
   __shared__ double sglx[kMaxGL], sglw[kMaxGL];
   __shared__ double2 sltab[kLogEntries];
   for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
@@ -1492,8 +1509,6 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* cc = scc[wid];
   double* F = sF[wid];
-  double* Eb = sE[wid];
-  double* Ec = sE[wid] + NP;
   unsigned long long my_panels = 0, my_degen = 0;
   for (int64_t it = (int64_t)blockIdx.x * SELF_WARPS + wid; it < n_items;
        it += (int64_t)gridDim.x * SELF_WARPS) {
@@ -1511,59 +1526,80 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     const double2 tp = txy[t];
     const double tx = tp.x, ty = tp.y;
     const ElemRec& Er = el[e];
-    double txi, teta;
-    rn_locate(Er, tx, ty, txi, teta);
     __syncwarp();
     for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
-    __syncwarp();
-    double acc = 0.0;
-    long long npan_item = 0;
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
+    if (lane < 3) {
       // side (A, B) = (v_k, v_{k+1}); reference corners (0,0), (1,0), (0,1)
+      const int k = lane;
+      double txi, teta;
+      rn_locate(Er, tx, ty, txi, teta);
       const double Ax = k == 0 ? Er.x0 : (k == 1 ? Er.x1 : Er.x2);
       const double Ay = k == 0 ? Er.y0 : (k == 1 ? Er.y1 : Er.y2);
       const double Bx = k == 0 ? Er.x1 : (k == 1 ? Er.x2 : Er.x0);
       const double By = k == 0 ? Er.y1 : (k == 1 ? Er.y2 : Er.y0);
       SelfGeom G;
       self_geom(tx, ty, Ax, Ay, Bx, By, G);
-      if (G.degenerate) {
+      const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
+      SelfSide& S = sS[wid][k];
+      S.Ax = G.Ax; S.Ay = G.Ay; S.ABx = G.ABx; S.ABy = G.ABy; S.L = G.L; S.h = G.h; S.st = G.st;
+      S.avx = Arx - txi;  // A - v in reference coordinates
+      S.avy = Ary - teta;
+      S.BRx = (k == 0 ? 1.0 : 0.0) - Arx;
+      S.BRy = (k == 1 ? 1.0 : 0.0) - Ary;
+      S.N = G.N; S.Mr = G.Mr; S.npan = min(G.npan, kMaxSelfPanels); S.degenerate = G.degenerate ? 1 : 0;
+    }
+    double txi, teta;
+    rn_locate(Er, tx, ty, txi, teta);
+    __syncwarp();
+    // (1) f at the M Fekete-type samples y = v + r (A - v) + s (B - A) of each
+    // sub-triangle (f has total degree <= p in (r, s)); the 3 M points of the
+    // target in one pass, SNPT per lane (degenerate sides are computed and
+    // not used)
+    for (int i = SNPT * lane; i < M3; i += 32 * SNPT) {
+      double xs[SNPT], ys[SNPT], f[SNPT];
+#pragma unroll
+      for (int q = 0; q < SNPT; ++q) {
+        const int iq = min(i + q, M3 - 1);
+        const int k = iq >= 2 * M ? 2 : (iq >= M ? 1 : 0), sq_ = iq - k * M;
+        const SelfSide& S = sS[wid][k];
+        xs[q] = fma(sss[sq_], S.BRx, fma(ssr[sq_], S.avx, txi));
+        ys[q] = fma(sss[sq_], S.BRy, fma(ssr[sq_], S.avy, teta));
+      }
+      density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
+#pragma unroll
+      for (int q = 0; q < SNPT; ++q)
+        if (i + q < M3) F[i + q] = f[q];
+    }
+    __syncwarp();
+    // (2) the sigma polynomials of the GGQ-rule moments per side, (Eb, Ec) =
+    // T2 f (Gauss-Legendre grid interpolation, Legendre transforms in r and
+    // sigma and the moment contraction, folded on the host)
+    for (int o = lane; o < 3 * 2 * NP; o += 32) {
+      const int k = o >= 4 * NP ? 2 : (o >= 2 * NP ? 1 : 0), oo = o - k * 2 * NP;
+      const double* Fk = F + k * M;
+      double sum = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < M; ++q) sum = fma(sT2[oo * M + q], Fk[q], sum);
+      sE[wid][k][oo] = sum;
+    }
+    __syncwarp();
+    double acc = 0.0;
+    long long npan_item = 0;
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      const SelfSide& S = sS[wid][k];
+      if (S.degenerate) {
         ++my_degen;  // identical in every lane; counted once below
         continue;
       }
-      const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
-      const double BRx = (k == 0 ? 1.0 : 0.0) - Arx, BRy = (k == 1 ? 1.0 : 0.0) - Ary;
-      const double avx = Arx - txi, avy = Ary - teta;  // A - v in reference coordinates
-      // (1) f at the M Fekete-type samples y = v + r (A - v) + s (B - A) of the
-      // sub-triangle (f has total degree <= p in (r, s)), SNPT per lane (one
-      // round of the warp for p <= 10)
-      for (int i = SNPT * lane; i < M; i += 32 * SNPT) {
-        double xs[SNPT], ys[SNPT], f[SNPT];
-#pragma unroll
-        for (int q = 0; q < SNPT; ++q) {
-          const int iq = min(i + q, M - 1);
-          xs[q] = fma(sss[iq], BRx, fma(ssr[iq], avx, txi));
-          ys[q] = fma(sss[iq], BRy, fma(ssr[iq], avy, teta));
-        }
-        density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
-#pragma unroll
-        for (int q = 0; q < SNPT; ++q)
-          if (i + q < M) F[i + q] = f[q];
-      }
-      __syncwarp();
-      // (2) the sigma polynomials of the GGQ-rule moments, (Eb, Ec) = T2 f
-      // (= Gauss-Legendre grid interpolation, Legendre transforms in r and
-      // sigma and the moment contraction, folded on the host)
-      for (int o = lane; o < 2 * NP; o += 32) {
-        double sum = 0.0;
-#pragma unroll 5
-        for (int q = 0; q < M; ++q) sum = fma(sT2[o * M + q], F[q], sum);
-        sE[wid][o] = sum;
-      }
-      __syncwarp();
-      // (5) arc-length nodes: dyadic panels x Gauss-Legendre;
+      SelfGeom G;
+      G.Ax = S.Ax; G.Ay = S.Ay; G.ABx = S.ABx; G.ABy = S.ABy; G.L = S.L; G.h = S.h; G.st = S.st;
+      G.N = S.N; G.Mr = S.Mr;
+      const double* Eb = sE[wid][k];
+      const double* Ec = Eb + NP;
+      // (3) arc-length nodes: dyadic panels x Gauss-Legendre;
       // the panel boundaries once per side in shared memory
-      const int npan = min(G.npan, kMaxSelfPanels);
+      const int npan = S.npan;
       for (int i = lane; i <= npan; i += 32) sB[wid][i] = self_bnd(G, i);
       __syncwarp();
       const int nodes = npan * NL;
@@ -1634,6 +1670,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   }
   if (lane == 0 && my_degen) atomicAdd(&stats[4], my_degen);
 }
+inline size_t self_dyn_smem(int p) { return sizeof(double) * 2 * (p + 1) * koorn_size(p); }
 
 // ---------------------------------------------------------------------------
 // Curved elements (oracle near_rec / self_eval_curved).
@@ -2593,7 +2630,7 @@ template <int P>
 void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
                  double* corr, double* sub, int64_t* panels) {
   const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
-  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, 0, c->stream>>>(
+  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->stream>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
       c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
       sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c));
@@ -3286,6 +3323,19 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_near_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cg<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cache_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)near_cache_mma_smem(kMaxModes)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(0)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(1)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(2)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(3)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(4)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(5)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(6)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(7)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(8)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(9)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
