@@ -42,6 +42,19 @@ sys.path.insert(0, HERE)
 # (profiles/r01_fp64_flops_config2.json) must agree: flop_per_pair_ncu.
 FAR_FLOP_PER_PAIR = 17
 FP64_FLOPS_PROFILE = os.path.join(HERE, "profiles", "r01_fp64_flops_config2.json")
+# SURVEY.md §8(d) frozen algorithmic work of the near and self pairs (a direct
+# implementation: Koornwinder evaluation at every leaf / panel node), with
+# K_p the counted cost of one Koornwinder evaluation
+SURVEY_KP = {4: 117, 6: 226, 8: 371, 12: 769}
+
+
+def survey_near_self_flops(st, p, len_q, len_n=49, n_l=16, n_g1=9):
+    kp = SURVEY_KP.get(p)
+    if kp is None:
+        return None
+    m2 = (p + 1) * (p + 2)
+    return (st["n_leaves"] * len_n * (m2 + 60) + st["n_near_pairs"] * len_q * 51
+            + st["n_panels"] * n_l * (60 + n_g1 * (kp + m2 + 10)) + st["n_self"] * len_q * 51)
 # SURVEY.md §8(d)'s frozen figure counted the libdevice log (51 flops/pair);
 # reported beside the roofline for comparison.
 SURVEY_FAR_FLOP_PER_PAIR = 51
@@ -369,12 +382,17 @@ def main():
         roof_near = {"bound": "fp64", "kernels": "near + self stages (" + ", ".join(prof_fl["near_stage_kernels"]) + ")",
                      "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
                      "flop_per_step": nf, "stage_ms": pair_ms,
-                     "flop_source": "ncu SASS dfma/dadd/dmul counts, profiles/r01_fp64_flops_config2.json",
+                     "flop_source": "ncu SASS dfma/dadd/dmul/DMMA counts, profiles/r01_fp64_flops_config2.json",
                      "per_kernel_frac_ncu": {k: round(v["fp64_flops"] / (v["ncu_ms"] * 1e-3) / 1e12 / peak, 3)
                                              for k, v in prof_fl["kernels"].items()
                                              if k in prof_fl["near_stage_kernels"] and v["fp64_flops"] > 1e9}}
     else:
         kf = None
+    sfl = survey_near_self_flops(stats[-1], pr.p, pr_len_q(pr), len(pr.rules.near[0]), len(pr.rules.gl[0]),
+                                 len(pr.rules.ggq[0]))
+    if roof_near is not None and sfl is not None:
+        roof_near["survey_flop_per_step"] = sfl
+        roof_near["survey_equiv_tflops"] = sfl / (pair_ms * 1e-3) / 1e12
 
     if rank == 0:
         s0 = stats[-1]
@@ -435,6 +453,11 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pr_len_q(pr):
+    """far-rule length of a problem (the sources per element)"""
+    return int(len(pr.rules.far[0]))
 
 
 def ctypes_ptr(t, ptype):
