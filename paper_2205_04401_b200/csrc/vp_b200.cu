@@ -1309,6 +1309,108 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
   }
 }
 
+// K4b cached leaves, evaluation form with 8 LANES PER LEAF: lane l works on
+// leaf l / 8 of a group of 4 and on its rule nodes (l mod 8) + 8 k, k < K8 =
+// ceil(len_n / 8) (49 nodes: 7 slots, 49 of 56 used, 88 %).  A lane reads its
+// leaf's D0 / BA / CA and cache-row address once per group (4 shared loads
+// for K8 nodes, against 4 per node in k_near_cg) and the G values of its K8
+// nodes (8 consecutive doubles per leaf and slot) a group ahead.  Same zero
+// rows past a batch and the same fixed summation order per target.
+template <int K8>
+__global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
+    k_near_c8(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
+              const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
+              const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
+              const double* __restrict__ gcache, const double* __restrict__ zrow,
+              const double* __restrict__ slot_ref, int cache_depth, double* __restrict__ part_t, unsigned c3ff) {
+  extern __shared__ __align__(16) unsigned char nsm[];
+  double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
+  __shared__ LeafRows sR;
+  const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
+  for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
+  for (int i = threadIdx.x; i < NG_WARPS * kLeafRows; i += blockDim.x) {
+    (&sR.d0[0][0])[i] = (&sR.ba[0][0])[i] = (&sR.ca[0][0])[i] = make_double2(0.0, 0.0);
+    (&sR.g[0][0])[i] = make_ulonglong2((unsigned long long)zrow, 0ull);
+  }
+  const int Ln = R->len_n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lg = lane >> 3, n0 = lane & 7;
+  double nu[K8], nv[K8];
+  bool nok[K8];
+#pragma unroll
+  for (int k = 0; k < K8; ++k) {
+    const int n = n0 + 8 * k;
+    nok[k] = n < Ln;
+    nu[k] = nok[k] ? R->near_x[n] : 0.0;
+    nv[k] = nok[k] ? R->near_y[n] : 0.0;
+  }
+  __syncthreads();
+  const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
+    const int64_t q0 = toff[t], q1 = toff[t + 1];
+    double acc = 0.0;
+    if (q1 > q0) {
+      const int64_t L0 = loff[q0], L1 = loff[q1];
+      const double2 tp = txy[t];
+      const double tx = tp.x, ty = tp.y;
+      int64_t q = q0;  // this lane's current pair (leaves ascend with the lane's batches)
+      for (int64_t lb = L0; lb < L1; lb += 32) {
+        const int nb = (int)min((int64_t)32, L1 - lb);
+        __syncwarp();
+        if (lane < nb) {
+          const int64_t Lf = lb + lane;
+          while (loff[q + 1] <= Lf) ++q;
+          const int32_t e = pair_elem[q];
+          const unsigned long long code = leaves[Lf];
+          const int d = (int)(code >> 58);
+          const ElemRec& Er = el[e];
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const double* r = slot_ref + 6 * slot;
+          const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
+          const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
+          sR.d0[wid][lane] = make_double2(tx - pax, ty - pay);
+          sR.ba[wid][lane] = make_double2(fma(r[3], Er.e2x, r[2] * Er.e1x), fma(r[3], Er.e2y, r[2] * Er.e1y));
+          sR.ca[wid][lane] = make_double2(fma(r[5], Er.e2x, r[4] * Er.e1x), fma(r[5], Er.e2y, r[4] * Er.e1y));
+          sR.g[wid][lane] = make_ulonglong2((unsigned long long)(gcache + ((int64_t)e * nslot + slot) * Ln), 0ull);
+        } else if (lane < nb + 4) {  // zero rows after the batch (rows 32.. stay zero)
+          sR.d0[wid][lane] = sR.ba[wid][lane] = sR.ca[wid][lane] = make_double2(0.0, 0.0);
+          sR.g[wid][lane] = make_ulonglong2((unsigned long long)zrow, 0ull);
+        }
+        __syncwarp();
+        double gn[K8];
+        {
+          const double* gr = reinterpret_cast<const double*>(sR.g[wid][lg].x) + n0;
+#pragma unroll
+          for (int k = 0; k < K8; ++k) gn[k] = nok[k] ? __ldg(gr + 8 * k) : 0.0;
+        }
+#pragma unroll 1
+        for (int li = 0; li < nb; li += 4) {
+          double g[K8];
+#pragma unroll
+          for (int k = 0; k < K8; ++k) g[k] = gn[k];
+          const int row = li + lg;
+          const double2 d0 = sR.d0[wid][row], ba = sR.ba[wid][row], ca = sR.ca[wid][row];
+          if (li + 4 < nb) {
+            const double* gr = reinterpret_cast<const double*>(sR.g[wid][row + 4].x) + n0;
+#pragma unroll
+            for (int k = 0; k < K8; ++k) gn[k] = nok[k] ? __ldg(gr + 8 * k) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < K8; ++k) {
+            if (k + 1 < K8 || nok[k]) {
+              const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
+              const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
+              acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
+            }
+          }
+        }
+      }
+    }
+    const double val = warp_sum(acc);
+    if (lane == 0) part_t[t] = val;
+  }
+}
+
 // Point sums of subtract-and-add for the per-pair API: part_s[p] =
 // sum_{i in T} q_i log r_{t,i}^2 (coincident pairs exactly 0);
 // warp per pair, lanes over T's sources.
@@ -2465,6 +2567,16 @@ inline int near_group_shape(int Ln, int* S_out) {
   return bestG;
 }
 
+template <int K8>
+void launch_near_c8(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
+                    const double* gc) {
+  const int blocks = (int)std::min<int64_t>(nblk(T, NG_WARPS), (int64_t)c->sm_count * 24);
+  k_near_c8<K8><<<std::max(blocks, 1), NG_WARPS * 32, sizeof(LogTab), c->stream>>>(
+      T, toff, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
+      c->d_rules.as<RulesDev>(), gc, gc + c->n_tri * (int64_t)(((1ll << (2 * (c->cache_depth + 1))) - 1) / 3) *
+      c->rules.len_n, c->d_slotref.as<double>(), c->cache_depth, c->d_neart.as<double>(), 0x3ff00000u);
+}
+
 template <int S>
 void launch_near_cg(vp_ctx* c, int G, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
                     const double* gc) {
@@ -2503,7 +2615,11 @@ void launch_near_int(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* p
     int S = 0;
     const int G = near_group_shape(c->rules.len_n, &S);
     static const bool force_ct = getenv("VP_NEAR_CT") != nullptr;  // A/B switch: one-leaf layout
-    if (G > 0 && !force_ct) {
+    static const bool force_cg = getenv("VP_NEAR_CG") != nullptr;  // A/B switch: leaf-group layout
+    const int K8 = (c->rules.len_n + 7) / 8;
+    if (K8 <= 8 && !force_ct && !force_cg) {
+      VP_DISPATCH_K(K8, launch_near_c8, c, T, toff, pelem, txy, gc);
+    } else if (G > 0 && !force_ct) {
       switch (S) {
         case 1: launch_near_cg<1>(c, G, T, toff, pelem, txy, gc); break;
         case 2: launch_near_cg<2>(c, G, T, toff, pelem, txy, gc); break;
@@ -3336,6 +3452,14 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_self<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||

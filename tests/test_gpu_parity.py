@@ -423,11 +423,12 @@ np.save({out!r}, u)
 """
 
 
-@pytest.mark.parametrize("env", [{"VP_NEAR_CT": "1"}, {"VP_NEAR_CACHE_SIMT": "1"}])
+@pytest.mark.parametrize("env", [{"VP_NEAR_CT": "1"}, {"VP_NEAR_CG": "1"}, {"VP_NEAR_CACHE_SIMT": "1"}])
 def test_near_kernel_variants_agree(tmp_path, env):
-    """The one-leaf cached-leaf kernel (k_near_ct) and the DFMA near-cache
-    contraction (k_near_cache) -- the A/B alternatives of k_near_cg and the
-    DMMA k_near_cache_mma -- give the same u up to summation order."""
+    """The one-leaf and leaf-group cached-leaf kernels (k_near_ct, k_near_cg)
+    and the DFMA near-cache contraction (k_near_cache) -- the A/B
+    alternatives of k_near_c8 and the DMMA k_near_cache_mma -- give the same
+    u up to summation order."""
     import os
     import subprocess
     import sys
