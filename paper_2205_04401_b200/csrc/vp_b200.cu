@@ -3470,15 +3470,15 @@ int vp_create(int device, vp_ctx** out) {
   }
   double2 lt[kLogEntries];
   log_table_fill(lt);
-  static double2 ltf[kFarLogEntries];
-  log_table_fill(ltf, kFarLogEntries);
+  std::vector<double2> ltf(kFarLogEntries);  // per call: vp_create may run on several threads
+  log_table_fill(ltf.data(), kFarLogEntries);
   double la[kMaxCurveDeg + 1], lb[kMaxCurveDeg + 1];
   for (int k = 0; k <= kMaxCurveDeg; ++k) {
     la[k] = leg_la(k);
     lb[k] = leg_lb(k);
   }
   if (cudaMemcpyToSymbol(g_logtab, lt, sizeof(lt)) != cudaSuccess ||
-      cudaMemcpyToSymbol(g_fartab, ltf, sizeof(ltf)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_fartab, ltf.data(), sizeof(double2) * ltf.size()) != cudaSuccess ||
       cudaMemcpyToSymbol(c_cn, cn, sizeof(cn)) != cudaSuccess ||
       cudaMemcpyToSymbol(c_leg_la, la, sizeof(la)) != cudaSuccess ||
       cudaMemcpyToSymbol(c_leg_lb, lb, sizeof(lb)) != cudaSuccess) {
