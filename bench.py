@@ -8,11 +8,12 @@ direct far sum, K4 near pairs, K5 self pairs, assembly) over one batch of
 targets: BASELINE config 2 (unit disk, 4,096 triangles, p=8, q=16, 184,320
 staggered targets, seeded synthetic density) unless --config says otherwise.
 
-Multi-GPU (torchrun, one process per GPU): weak scaling.  Rank r evaluates
-its own batch -- config 2's staggered target mesh rotated by r/N of the
-finest angular cell -- with mesh and density replicated; the only
-collective is the NCCL all-gather of u (north_star).  Timing is on the
-device (CUDA events) and the reported time is the max over ranks.
+Multi-GPU (torchrun, one process per GPU): weak scaling.  The job's targets
+are N copies of config 2's staggered target mesh, copy r rotated by r/N of
+the finest angular cell; they are Morton-ordered and cut into N contiguous
+equal shards (paper_2205_04401_b200.dist), mesh and density replicated, and
+the only collective is the NCCL all-gather of u (north_star).  Timing is on
+the device (CUDA events) and the reported time is the max over ranks.
 
 --impl reference times the CPU oracle (oracle/, a restatement of the
 reference's specified path; the reference itself has no implementation of
@@ -89,15 +90,36 @@ def rotate(txy, theta):
     return np.stack([c * txy[:, 0] - s * txy[:, 1], s * txy[:, 0] + c * txy[:, 1]], 1)
 
 
-def rank_targets(pr, rank, world):
-    """Weak-scaling batch of rank r: config targets rotated by r/world of the
-    finest angular cell (disk configs) or shifted by r/world of a cell width."""
-    if world == 1 or rank == 0:
+def job_targets(pr, world):
+    """The whole job's targets for weak scaling: world copies of the config's
+    target set, copy r rotated by r/world of the finest angular cell (disk
+    configs) or shifted by r/world of a cell width, so every GPU gets a
+    config-sized batch of distinct targets."""
+    if world == 1:
         return pr.txy.copy()
-    if pr.config == 2:
-        return rotate(pr.txy, 2 * np.pi / (16 * 16) * rank / world)
-    h = np.sqrt(2.0 / pr.n_tri)
-    return pr.txy + np.array([h * rank / world * 0.37, h * rank / world * 0.21])
+    parts = []
+    for r in range(world):
+        if r == 0:
+            parts.append(pr.txy)
+        elif pr.config == 2:
+            parts.append(rotate(pr.txy, 2 * np.pi / (16 * 16) * r / world))
+        else:
+            h = np.sqrt(2.0 / pr.n_tri)
+            parts.append(pr.txy + np.array([h * r / world * 0.37, h * r / world * 0.21]))
+    return np.concatenate(parts)
+
+
+def rank_targets(pr, rank, world):
+    """This rank's shard (north_star): the job's targets in
+    Morton order, cut into contiguous equal-count shards
+    (paper_2205_04401_b200.dist); mesh and density are replicated."""
+    from paper_2205_04401_b200.dist import morton_order, shard_bounds
+    U = job_targets(pr, world)
+    if world == 1:
+        return U, len(U)
+    order = morton_order(U)
+    lo, hi = shard_bounds(len(U), rank, world)
+    return U[order[lo:hi]], len(U)
 
 
 class ClockSampler:
@@ -228,6 +250,7 @@ def main():
     args = parse()
     rank, world, local = dist_env()
     import paper_2205_04401_b200 as vp
+    from paper_2205_04401_b200.dist import gather_potentials
     pr = vp.load_config(args.config, args.q, args.seed)
     if args.impl == "reference":
         run_reference(args, pr, rank, world)
@@ -241,18 +264,16 @@ def main():
     dev = torch.device("cuda", local)
     ev = vp.Evaluator(local).load(pr)
     ev.set_far_method(args.far)
-    txy_h = rank_targets(pr, rank, world)
+    txy_h, T_job = rank_targets(pr, rank, world)
     T = txy_h.shape[0]
     d_txy = torch.from_numpy(txy_h).to(dev).contiguous()
     d_u = torch.empty(T, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
-    gathered = torch.empty(world * T, dtype=torch.float64, device=dev) if world > 1 else None
-
     def step():
         st = ev.evaluate_device(T, d_txy.data_ptr(), d_u.data_ptr(), stream.cuda_stream)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, d_u)
+        if world > 1:  # the only collective: gather of u (NCCL all-gather of padded shards)
+            gather_potentials(d_u, T_job, rank, world)
         return st
 
     clk = ClockSampler(local)
@@ -286,7 +307,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
-    value = world * T * args.steps / (ms_total * 1e-3)
+    value = T_job * args.steps / (ms_total * 1e-3)  # the whole job's targets
 
     # far kernel (dominant) roofline from the library's device events
     S = stats[-1]["n_sources"]
@@ -328,7 +349,7 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-        e2e = {"value": world * T * args.steps / dt, "unit": "targets/s",
+        e2e = {"value": T_job * args.steps / dt, "unit": "targets/s",
                "h2d_bytes_per_step": int(pr.coeffs.nbytes + txy_h.nbytes),
                "d2h_bytes_per_step": int(8 * T)}
 
@@ -356,7 +377,7 @@ def main():
             dist.all_reduce(ta, op=dist.ReduceOp.MAX)
         a_ms = float(ta.item())
         diff = float((d_u - u_ref).abs().max().item() / u_ref.abs().max().item())
-        alt = {"far_method": other, "value": world * T * args.steps / (a_ms * 1e-3),
+        alt = {"far_method": other, "value": T_job * args.steps / (a_ms * 1e-3),
                "ms_per_step": a_ms / args.steps,
                "far_ms": float(np.mean([s["t_far_ms"] for s in a_st])),
                "fmm_levels": a_st[-1]["fmm_levels"], "fmm_order": 31,

@@ -63,3 +63,23 @@ def test_gloo_two_rank_gather_is_bit_identical(tmp_path):
     pr = vp.load_config(1)
     u1, _, _ = Oracle.from_problem(pr).evaluate(pr.txy[::3], nthreads=2)
     assert np.array_equal(np.load(out), u1)
+
+
+def test_bench_shards_partition_the_job():
+    """bench.py's weak-scaling shards (Morton order, contiguous equal counts)
+    cover the job's targets exactly once, and at N=1 the job is config 2."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2205_04401_b200 as vp
+    pr = vp.load_config(2, with_rules=False)
+    t1, n1 = bench.rank_targets(pr, 0, 1)
+    assert n1 == pr.n_tgt and np.array_equal(t1, pr.txy)
+    for world in (2, 4):
+        U = bench.job_targets(pr, world)
+        shards = [bench.rank_targets(pr, r, world) for r in range(world)]
+        assert all(n == len(U) == world * pr.n_tgt for _, n in shards)
+        assert all(len(s) == pr.n_tgt for s, _ in shards)
+        got = np.concatenate([s for s, _ in shards])
+        key = lambda a: a[np.lexsort((a[:, 1], a[:, 0]))]
+        assert np.array_equal(key(got), key(U))
