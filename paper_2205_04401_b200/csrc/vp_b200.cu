@@ -2303,6 +2303,7 @@ struct vp_ctx {
   int64_t free_mem_at_first_near = -1;
   int tabs_p = -1;  // p of the density-independent tables (K1's V, near-cache Vt, SelfTab); -1: stale
   int cacheV_depth = -2, cacheV_p = -1;
+  DevBuf f_tk, f_tk2, f_tv, f_tord;  // FMM: target leaf keys and the leaf order of the targets
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
   // far field on its own stream and host thread when it overlaps the near and
@@ -3178,17 +3179,29 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
       k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
                                                             c->f_lp.as<double2>());
   }
-  // L2P + P2P
+  // L2P + P2P over the targets in leaf order (stable radix sort by leaf key)
   CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tk.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tk2.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tv.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tord.ensure(sizeof(int32_t) * (T + 1)));
+  k_fmm_tkeys<<<nblk(T, 256), 256, 0, c->fs>>>(T, txy, g, c->f_tk.as<int32_t>(), c->f_tv.as<int32_t>());
+  tmpb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(), c->f_tv.as<int32_t>(),
+                                  c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
+  CUDA_TRY(c, c->f_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->f_tmp.p, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(),
+                                  c->f_tv.as<int32_t>(), c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
   const size_t sm_eval = sizeof(LogTab);
   if (zero_check)
     k_fmm_eval<true><<<nblk(T, 256), 256, sm_eval, c->fs>>>(
         T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
-        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
+        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u, c->f_tord.as<int32_t>());
   else
     k_fmm_eval<false><<<nblk(T, 256), 256, sm_eval, c->fs>>>(
         T, txy, g, c->f_beg.as<int64_t>(), c->f_end.as<int64_t>(), c->f_pxy.as<double2>(), c->f_pq.as<double>(),
-        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u);
+        c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u, c->f_tord.as<int32_t>());
+  c->far_launches += 3;
   CUDA_TRY(c, cudaGetLastError());
   c->far_launches += 7 + 2 * (L - 1);
   // targets outside the root box: direct far sum

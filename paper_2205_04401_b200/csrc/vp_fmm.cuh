@@ -137,6 +137,21 @@ __global__ void k_fmm_keys(int64_t S, const double* __restrict__ sx, const doubl
   vals[i] = (int32_t)i;
 }
 
+// leaf key of every target (row-major leaf index; n*n for targets outside the
+// root box), for the leaf-ordered L2P + P2P pass
+__global__ void k_fmm_tkeys(int64_t T, const double2* __restrict__ txy, FmmGeom g, int32_t* __restrict__ keys,
+                            int32_t* __restrict__ vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int n = 1 << g.L;
+  const double inv_h = (double)n / g.h0;
+  const double2 z = txy[t];
+  const double fx = floor((z.x - g.x0) * inv_h), fy = floor((z.y - g.y0) * inv_h);
+  const bool in = fx >= 0.0 && fy >= 0.0 && fx < (double)n && fy < (double)n;
+  keys[t] = in ? (int)fy * n + (int)fx : n * n;
+  vals[t] = (int32_t)t;
+}
+
 __global__ void k_fmm_gather(int64_t S, const int32_t* __restrict__ idx, const double* __restrict__ sx,
                              const double* __restrict__ sy, const double* __restrict__ sq,
                              double2* __restrict__ pxy, double* __restrict__ pq) {
@@ -448,14 +463,17 @@ __global__ void __launch_bounds__(256)
     k_fmm_eval(int64_t T, const double2* __restrict__ txy, FmmGeom g, const int64_t* __restrict__ beg,
                const int64_t* __restrict__ end, const double2* __restrict__ pxy,
                const double* __restrict__ pq, const double2* __restrict__ lp, double* __restrict__ u,
-               int32_t* __restrict__ flag, unsigned c3ff) {
+               int32_t* __restrict__ flag, unsigned c3ff, const int32_t* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char fsm[];
   double2* ltab = reinterpret_cast<double2*>(fsm);
   for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) ltab[i] = g_logtab[i / kLogCopies];
   __syncthreads();
   const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
+  // targets in leaf order (`order`, a stable sort by leaf key): a warp's
+  // threads share their leaf, so the expansion and source loads broadcast
+  const int64_t ti = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ti >= T) return;
+  const int64_t t = order ? (int64_t)order[ti] : ti;
   const double2 z = txy[t];
   const int n = 1 << g.L, P1 = g.p + 1;
   const double inv_h = (double)n / g.h0, h = g.h0 / n;
