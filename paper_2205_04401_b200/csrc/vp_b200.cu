@@ -588,6 +588,13 @@ struct LeafOut {
 // whose pair is done take the chunk's next pair (ballot + prefix count: the
 // assignment is warp-synchronous, and a pair's outputs do not depend on it).
 constexpr int kLeafChunk = 128;
+// per-pair leaf scratch of the count pass: pairs with more leaves are walked
+// again (k_near_leaves<true>); 256 leaves per pair leaves none over on config 2
+// (the scratch is written sparsely, only the leaves that exist)
+#ifndef VP_LEAF_SCRATCH_MAX
+#define VP_LEAF_SCRATCH_MAX 256
+#endif
+constexpr int kLeafScratchMax = VP_LEAF_SCRATCH_MAX;
 template <bool FILL>
 __global__ void __launch_bounds__(128)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
@@ -2681,7 +2688,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
     c->free_mem_at_first_near = (int64_t)free_b;
   }
   const int64_t budget = std::max<int64_t>(c->leaf_scratch_budget, c->free_mem_at_first_near / 10);
-  const int cap = (int)std::min<int64_t>(64, (budget / 8) / std::max<int64_t>(n, 1));
+  const int cap = (int)std::min<int64_t>(kLeafScratchMax, (budget / 8) / std::max<int64_t>(n, 1));
   CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
   CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
