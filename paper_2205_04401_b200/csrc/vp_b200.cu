@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(128)
           side_lengths0(E, l0);
           gd = -1;
           sp = 0;
-          stack[sp++] = 0ull;
+          stack[sp++] = ball_factor == 0.0 ? (1ull << 57) : 0ull;  // precise model: root untested
           n = nc = 0;
           if (FILL) {
             oc = lo.offc[p];
@@ -657,14 +657,109 @@ __global__ void __launch_bounds__(128)
       continue;
     }
     if (!act) continue;
-    // one node of this lane's pair
+    bool bad = false;
+    if (ball_factor == 0.0) {
+      // precise model: one step expands a rejected node, testing its four
+      // children together.  The children's 12 vertex distances are 6 distinct
+      // ones (a, b, c, m_ab, m_bc, m_ca; a shared vertex has the same
+      // reference coordinates, hence bit-identical distance), so a child test
+      // costs 1.5 square roots instead of 3.  Accepted children are emitted in
+      // child order, rejected ones pushed (child 0 on top); the leaf set and
+      // the counters are those of near_accept node by node.  The root is
+      // tested first (`code` bit 57 marks a node not tested yet).
+      const unsigned long long code = stack[--sp];
+      const int d = (int)(code >> 58);
+      // (a depth-0 code has path 0, so bit 57 can mark it; deeper paths use it)
+      const bool untested_root = d == 0 && (code & (1ull << 57));
+      const unsigned long long path = untested_root ? 0ull : code & kPathMask;
+      double ax, ay, bx, by, cx, cy;
+      decode_path_i(path, d, ax, ay, bx, by, cx, cy);
+      if (untested_root) {
+        bool le1;
+        if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[0]), ax, ay, bx, by, cx, cy, le1, 0, 0.0, l0, gd, gv)) {
+          if (FILL) {
+            if (0 <= lo.D) lo.leafc[oc++] = 0ull;
+            else lo.leafd[od++] = 0ull;
+          } else if (n < cap) {
+            scratch[p * cap + n] = 0ull;
+          }
+          ++n;
+          nc += 0 <= lo.D ? 1 : 0;
+          rle1 += le1 ? 1ull : 0ull;
+        } else {
+          stack[sp++] = 0ull;
+        }
+      } else {
+        const int dc = d + 1;
+        const double rd = rn_mul(E.rho0n, skd[dc]);
+        const unsigned long long base = ((unsigned long long)dc << 58) | (path << 2);
+        bool acc4[4];
+        const bool le1 = !(rd > 1.0);
+        if (le1) {
+          acc4[0] = acc4[1] = acc4[2] = acc4[3] = true;
+        } else {
+          if (dc != gd) {
+            gd = dc;
+            gv = rn_mul(rn_add(rd, rn_div(1.0, rd)), 0.5);
+          }
+          const double sc = ldexp(1.0, -dc);
+          double th[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) th[k] = rn_mul(gv, rn_mul(l0[k], sc));
+          // reference vertices a, b, c, m_ab, m_bc, m_ca (exact dyadics)
+          const double vx[6] = {ax, bx, cx, (ax + bx) * 0.5, (bx + cx) * 0.5, (cx + ax) * 0.5};
+          const double vy[6] = {ay, by, cy, (ay + by) * 0.5, (by + cy) * 0.5, (cy + ay) * 0.5};
+          double dv[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const double px = rn_add(E.x0, rn_add(rn_mul(vx[k], E.e1x), rn_mul(vy[k], E.e2x)));
+            const double py = rn_add(E.y0, rn_add(rn_mul(vx[k], E.e1y), rn_mul(vy[k], E.e2y)));
+            dv[k] = rn_dist(tx, ty, px, py);
+          }
+          // child vertex triples (decode_path order): 0 (a, m_ab, m_ca),
+          // 1 (m_ab, b, m_bc), 2 (m_ca, m_bc, c), 3 (m_bc, m_ca, m_ab)
+          constexpr int cv[4][3] = {{0, 3, 5}, {3, 1, 4}, {5, 4, 2}, {4, 5, 3}};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            bool in = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) in = in || (rn_add(dv[cv[j][k]], dv[cv[j][(k + 1) % 3]]) < th[k]);
+            acc4[j] = !in;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!acc4[j]) continue;
+          const unsigned long long cc = base | (unsigned long long)j;
+          if (FILL) {
+            if (dc <= lo.D) lo.leafc[oc++] = cc;
+            else lo.leafd[od++] = cc;
+          } else if (n < cap) {
+            scratch[p * cap + n] = cc;
+          }
+          ++n;
+          nc += dc <= lo.D ? 1 : 0;
+          rle1 += le1 ? 1ull : 0ull;
+          maxd = max(maxd, dc);
+        }
+#pragma unroll
+        for (int j = 3; j >= 0; --j) {
+          if (acc4[j]) continue;
+          if (dc + 1 > kMaxPathDepth || sp + 1 > kStackCap) {
+            bad = true;
+            break;
+          }
+          stack[sp++] = base | (unsigned long long)j;
+        }
+      }
+    } else {
+    // ball model: one node of this lane's pair per step
     const unsigned long long code = stack[--sp];
     const int d = (int)(code >> 58);
     const unsigned long long path = code & kPathMask;
     double ax, ay, bx, by, cx, cy;
     decode_path_i(path, d, ax, ay, bx, by, cx, cy);
     bool le1;
-    bool bad = false;
     if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd, gv)) {
       if (FILL) {
         if (d <= lo.D) lo.leafc[oc++] = code;
@@ -684,6 +779,7 @@ __global__ void __launch_bounds__(128)
       stack[sp++] = base | 2ull;
       stack[sp++] = base | 1ull;
       stack[sp++] = base;
+    }
     }
     if (bad || sp == 0) {  // the pair is done
       if (bad) atomicExch(err, 2);
