@@ -595,8 +595,11 @@ constexpr int kLeafChunk = 128;
 #define VP_LEAF_SCRATCH_MAX 256
 #endif
 constexpr int kLeafScratchMax = VP_LEAF_SCRATCH_MAX;
+#ifndef VP_LEAVES_MINB
+#define VP_LEAVES_MINB 5
+#endif
 template <bool FILL>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, VP_LEAVES_MINB)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
                   const int32_t* __restrict__ pair_elem, const double2* __restrict__ txy,
                   const ElemRec* __restrict__ el, const RulesDev* __restrict__ R,
