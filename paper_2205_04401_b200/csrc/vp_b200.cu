@@ -189,14 +189,16 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
                         int64_t* __restrict__ cnt_out, const int64_t* __restrict__ off,
                         int32_t* __restrict__ ids, double2* __restrict__ self_ref, CurvesDev CV,
                         const int32_t* __restrict__ tlist, int32_t* __restrict__ scratch, int cap,
-                        int32_t* __restrict__ over, unsigned* __restrict__ n_over) {
+                        int32_t* __restrict__ over, unsigned* __restrict__ n_over, int* __restrict__ nonfinite) {
   // count pass: also keeps the first `cap` ids of N(t) in scratch[t * cap ..]
-  // and lists the targets with more (walked again by the fill pass over tlist)
+  // and lists the targets with more (walked again by the fill pass over tlist);
+  // flags non-finite targets (the evaluation's input check, on the device)
   const int64_t ti = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (ti >= T) return;
   const int64_t t = tlist ? tlist[ti] : ti;
   const double2 p = txy[t];
   const double tx = p.x, ty = p.y;
+  if (nonfinite && !(isfinite(tx) && isfinite(ty))) *nonfinite = 1;
   int64_t b = 0, e = 0;
   const double fx = floor(rn_mul(rn_sub(tx, g.x0), g.inv_cs));
   const double fy = floor(rn_mul(rn_sub(ty, g.y0), g.inv_cs));
@@ -3347,6 +3349,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   CUDA_TRY(c, c->d_lsc.ensure(sizeof(int32_t) * (size_t)T * cap + 4));
   CUDA_TRY(c, c->d_tover.ensure(sizeof(int32_t) * (T + 1)));
   CUDA_TRY(c, c->d_ntover.ensure(sizeof(unsigned)));
+  CUDA_TRY(c, c->d_err.ensure(2 * sizeof(int)));  // [0] near-field limits, [1] non-finite target
   CUDA_TRY(c, cudaMemsetAsync(c->d_ntover.p, 0, sizeof(unsigned), c->stream));
   const GridDev G = c->grid;
   const int nan = (int)c->h_allnear.size();
@@ -3354,7 +3357,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
       T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
       c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c), nullptr,
-      c->d_lsc.as<int32_t>(), cap, c->d_tover.as<int32_t>(), c->d_ntover.as<unsigned>());
+      c->d_lsc.as<int32_t>(), cap, c->d_tover.as<int32_t>(), c->d_ntover.as<unsigned>(), c->d_err.as<int>() + 1);
   CUDA_TRY(c, cudaMemsetAsync(c->d_cnt.as<int64_t>() + T, 0, sizeof(int64_t), c->stream));
   size_t tmpb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
@@ -3372,7 +3375,8 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
     k_lists<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
         nover, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
         c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr, c->d_off.as<int64_t>(),
-        c->d_ids.as<int32_t>(), nullptr, curves_dev(c), c->d_tover.as<int32_t>(), nullptr, 0, nullptr, nullptr);
+        c->d_ids.as<int32_t>(), nullptr, curves_dev(c), c->d_tover.as<int32_t>(), nullptr, 0, nullptr, nullptr,
+        nullptr);
   CUDA_TRY(c, cudaGetLastError());
   c->last_launches += 3 + (nover > 0 ? 1 : 0);
   *n_ids_out = n_ids;
@@ -3382,9 +3386,9 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
 int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats* st) {
   c->last_launches = 0;
   CUDA_TRY(c, c->d_stats.ensure(sizeof(unsigned long long) * 8));
-  CUDA_TRY(c, c->d_err.ensure(sizeof(int)));
+  CUDA_TRY(c, c->d_err.ensure(2 * sizeof(int)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, 2 * sizeof(int), c->stream));
   cudaEvent_t* ev = c->ev;
   CUDA_TRY(c, cudaEventRecord(ev[0], c->stream));
   int64_t n_ids = 0;
@@ -3455,12 +3459,13 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
   CUDA_TRY(c, cudaGetLastError());
   unsigned long long hs[8];
-  int herr = 0;
+  int herr[2] = {0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(hs, c->d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(&herr, c->d_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(herr, c->d_err.p, sizeof(herr), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (herr) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits "
-                                 "(target effectively on element boundary)");
+  if (herr[1]) return set_err(c, 2, "evaluate: non-finite target coordinate");
+  if (herr[0]) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits "
+                                    "(target effectively on element boundary)");
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->n_targets = T;
@@ -3922,8 +3927,6 @@ int vp_evaluate(vp_ctx* c, int64_t n_tgt, const double* txy, double* u_out, vp_s
     if (st) std::memset(st, 0, sizeof(*st));
     return 0;
   }
-  for (int64_t i = 0; i < 2 * n_tgt; ++i)
-    if (!std::isfinite(txy[i])) return set_err(c, 2, "evaluate: non-finite target coordinate");
   CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n_tgt));
   CUDA_TRY(c, c->d_u.ensure(sizeof(double) * n_tgt));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_txy.p, txy, sizeof(double) * 2 * n_tgt, cudaMemcpyHostToDevice, c->stream));
@@ -3968,9 +3971,9 @@ static int pairs_common(vp_ctx* c, int64_t n, const double* txy, const int32_t* 
   CUDA_TRY(c, cudaSetDevice(c->device));
   if (int rc = compute_sources(c)) return rc;
   CUDA_TRY(c, c->d_stats.ensure(sizeof(unsigned long long) * 8));
-  CUDA_TRY(c, c->d_err.ensure(sizeof(int)));
+  CUDA_TRY(c, c->d_err.ensure(2 * sizeof(int)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_stats.p, 0, sizeof(unsigned long long) * 8, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_err.p, 0, 2 * sizeof(int), c->stream));
   CUDA_TRY(c, c->d_txy.ensure(sizeof(double) * 2 * n));
   CUDA_TRY(c, c->d_pelem.ensure(sizeof(int32_t) * n));
   CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * n));

@@ -440,3 +440,18 @@ def test_near_kernel_variants_agree(tmp_path, env):
                        env={**os.environ, **e}, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-13
+
+
+def test_nonfinite_target_is_a_numerical_error(cfg1):
+    """A NaN or infinite target coordinate fails the evaluation with code 2
+    (numerical failure; the check runs on the device in the list build), and
+    the context keeps working afterwards."""
+    pr, ev, O = cfg1
+    for bad in (np.nan, np.inf):
+        txy = pr.txy[:64].copy()
+        txy[17, 1] = bad
+        with pytest.raises(vp.NumericalError, match="non-finite"):
+            ev.evaluate(txy)
+    u, _ = ev.evaluate(pr.txy[:64])
+    u_o, _, _ = O.evaluate(pr.txy[:64])
+    assert rel(u, u_o) <= REL_TOL
