@@ -316,7 +316,8 @@ def main():
     peak, peak_src = fp64_peak()
     achieved = far_flop / (far_ms * 1e-3) / 1e12
     prof = load_json(os.path.join(HERE, "profiles", "far_kernel_traffic.json")) or {}
-    pair_ms = float(np.mean([s["t_near_ms"] + s["t_self_ms"] for s in stats]))
+    # pair stage: near chain (main stream) beside self + point sums (s3)
+    pair_ms = float(np.mean([s["t_pair_ms"] for s in stats]))
     n_pairs = stats[-1]["n_near_pairs"] + stats[-1]["n_self"]
 
     # e2e through the public API with pinned host buffers (set_density + evaluate)
@@ -450,9 +451,10 @@ def main():
                          "sources": float(np.mean([s["t_sources_ms"] for s in stats])),
                          "far": far_ms,
                          "near": float(np.mean([s["t_near_ms"] for s in stats])),
-                         "self": float(np.mean([s["t_self_ms"] for s in stats]))},
+                         "self": float(np.mean([s["t_self_ms"] for s in stats])),
+                         "pair_stage": pair_ms},
             # slowest step's stages (host round trips inside a stage show up here)
-            "split_ms_max": {k: float(max(s[f"t_{k}_ms"] for s in stats)) for k in ("list", "far", "near", "self")},
+            "split_ms_max": {k: float(max(s[f"t_{k}_ms"] for s in stats)) for k in ("list", "far", "near", "self", "pair")},
             "roofline": {"bound": "fp64", "kernel": "k_far (K2 direct far sum)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "peak_source": peak_src,

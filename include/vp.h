@@ -75,6 +75,8 @@ typedef struct {
   int32_t far_method;   /* 0 direct, 1 FMM */
   int32_t fmm_levels;   /* leaf level of the FMM quadtree */
   int64_t fmm_outside;  /* targets outside the FMM root box (summed directly) */
+  double t_pair_ms;     /* device time of the pair stage: near (K4), self (K5) and the
+                           point sums, which run side by side on two streams */
 } vp_stats;
 
 /* context (device = CUDA ordinal) */

@@ -44,6 +44,7 @@ class VpStats(ctypes.Structure):
         ("t_total_ms", ctypes.c_double), ("t_sources_ms", ctypes.c_double),
         ("t_far_kernel_ms", ctypes.c_double),
         ("far_method", ctypes.c_int32), ("fmm_levels", ctypes.c_int32), ("fmm_outside", ctypes.c_int64),
+        ("t_pair_ms", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -456,6 +456,14 @@ constexpr int kMaxPathDepth = 29;
 constexpr int NEAR_WARPS = 8;
 constexpr int kStackCap = 3 * kMaxPathDepth + 4;
 constexpr unsigned long long kPathMask = (1ull << 58) - 1ull;
+// A CACHED leaf (depth <= D <= 6, path <= 12 bits) also carries its element
+// id in bits 16..47, so the evaluation kernels read it with the code instead
+// of walking the pair offsets and pair_elem.
+constexpr unsigned long long kCPathMask = 0xFFFFull;
+__device__ __forceinline__ unsigned long long tag_cached(unsigned long long code, int32_t e) {
+  return code | ((unsigned long long)(uint32_t)e << 16);
+}
+__device__ __forceinline__ int32_t cached_elem(unsigned long long code) { return (int32_t)(uint32_t)(code >> 16); }
 
 __device__ __forceinline__ void decode_path(unsigned long long path, int d, double& ax, double& ay,
                                             double& bx, double& by, double& cx, double& cy) {
@@ -580,6 +588,7 @@ struct LeafOut {
   int32_t* deep;
   unsigned* n_deep;
   int D;
+  const int32_t* pelem;  // pair -> element, for the cached-leaf tag
 };
 
 // Load balance: leaf counts per pair vary from 1 to hundreds, so a thread
@@ -683,7 +692,7 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
         bool le1;
         if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[0]), ax, ay, bx, by, cx, cy, le1, 0, 0.0, l0, gd, gv)) {
           if (FILL) {
-            if (0 <= lo.D) lo.leafc[oc++] = 0ull;
+            if (0 <= lo.D) lo.leafc[oc++] = tag_cached(0ull, pair_elem[p]);
             else lo.leafd[od++] = 0ull;
           } else if (n < cap) {
             scratch[p * cap + n] = 0ull;
@@ -737,7 +746,7 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
           if (!acc4[j]) continue;
           const unsigned long long cc = base | (unsigned long long)j;
           if (FILL) {
-            if (dc <= lo.D) lo.leafc[oc++] = cc;
+            if (dc <= lo.D) lo.leafc[oc++] = tag_cached(cc, pair_elem[p]);
             else lo.leafd[od++] = cc;
           } else if (n < cap) {
             scratch[p * cap + n] = cc;
@@ -767,7 +776,7 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
     bool le1;
     if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd, gv)) {
       if (FILL) {
-        if (d <= lo.D) lo.leafc[oc++] = code;
+        if (d <= lo.D) lo.leafc[oc++] = tag_cached(code, pair_elem[p]);
         else lo.leafd[od++] = code;
       } else if (n < cap) {
         scratch[p * cap + n] = code;
@@ -819,9 +828,10 @@ __global__ void k_leaves_copy(int64_t n_pairs, const int64_t* __restrict__ cnt, 
   const int64_t n = cnt[p];
   if (n > cap) return;
   int64_t oc = lo.offc[p], od = lo.offd[p];
+  const int32_t e = lo.pelem[p];
   for (int64_t i = 0; i < n; ++i) {
     const unsigned long long code = scratch[p * cap + i];
-    if ((int)(code >> 58) <= lo.D) lo.leafc[oc++] = code;
+    if ((int)(code >> 58) <= lo.D) lo.leafc[oc++] = tag_cached(code, e);
     else lo.leafd[od++] = code;
   }
 }
@@ -1139,7 +1149,7 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
       if (mine) {
         const ElemRec& Er = el[e];
         const int pos = __popc(mm & lt_mask);
-        const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+        const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kCPathMask);
         const double* r = slot_ref + 6 * slot;  // a, b - a, c - a of the slot (L1-resident)
         const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
         const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
@@ -1238,7 +1248,7 @@ __global__ void __launch_bounds__(NC_WARPS * 32, 2)
           const unsigned long long code = leaves[Lf];
           const int d = (int)(code >> 58);
           const ElemRec& Er = el[e];
-          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kCPathMask);
           const double* r = slot_ref + 6 * slot;
           const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
           const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
@@ -1369,7 +1379,7 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
           const unsigned long long code = leaves[Lf];
           const int d = (int)(code >> 58);
           const ElemRec& Er = el[e];
-          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kCPathMask);
           const double* r = slot_ref + 6 * slot;
           const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
           const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
@@ -1456,23 +1466,23 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
   const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
   for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
     const int64_t q0 = toff[t], q1 = toff[t + 1];
-    double acc = 0.0;
+    double acc = 0.0, acc1 = 0.0;
     if (q1 > q0) {
       const int64_t L0 = loff[q0], L1 = loff[q1];
       const double2 tp = txy[t];
       const double tx = tp.x, ty = tp.y;
-      int64_t q = q0;  // this lane's current pair (leaves ascend with the lane's batches)
+      // the leaf codes carry their element (tag_cached); the next batch's
+      // codes are loaded while this batch computes
+      unsigned long long code_n = lane < L1 - L0 ? leaves[L0 + lane] : 0ull;
       for (int64_t lb = L0; lb < L1; lb += 32) {
         const int nb = (int)min((int64_t)32, L1 - lb);
+        const unsigned long long code = code_n;
         __syncwarp();
         if (lane < nb) {
-          const int64_t Lf = lb + lane;
-          while (loff[q + 1] <= Lf) ++q;
-          const int32_t e = pair_elem[q];
-          const unsigned long long code = leaves[Lf];
+          const int32_t e = cached_elem(code);
           const int d = (int)(code >> 58);
           const ElemRec& Er = el[e];
-          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kPathMask);
+          const int slot = ((1 << (2 * d)) - 1) / 3 + (int)(code & kCPathMask);
           const double* r = slot_ref + 6 * slot;
           const double pax = fma(r[1], Er.e2x, fma(r[0], Er.e1x, Er.x0));
           const double pay = fma(r[1], Er.e2y, fma(r[0], Er.e1y, Er.y0));
@@ -1484,6 +1494,7 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
           sR.d0[wid][lane] = sR.ba[wid][lane] = sR.ca[wid][lane] = make_double2(0.0, 0.0);
           sR.g[wid][lane] = make_ulonglong2((unsigned long long)zrow, 0ull);
         }
+        if (lb + 32 + lane < L1) code_n = leaves[lb + 32 + lane];
         __syncwarp();
         double gn[K8];
         {
@@ -1508,13 +1519,14 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
             if (k + 1 < K8 || nok[k]) {
               const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
               const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
-              acc = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), acc);
+              double& a = (k & 1) ? acc1 : acc;  // two chains: K8 DFMAs deep -> K8 / 2
+              a = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), a);
             }
           }
         }
       }
     }
-    const double val = warp_sum(acc);
+    const double val = warp_sum(acc + acc1);
     if (lane == 0) part_t[t] = val;
   }
 }
@@ -2389,7 +2401,7 @@ struct vp_ctx {
   DevBuf d_txy, d_u, d_ufar, d_part, d_self, d_cnt, d_off, d_ids, d_ptgt, d_corr, d_corr_self,
       d_selfref, d_stats, d_err, d_tmp, d_sub, d_leaves, d_pelem, d_lcnt, d_loff, d_leafcodes;
   int64_t n_leaves_last = 0;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};
   int last_launches = 0;
   // mesh bounding box (root of the FMM tree)
   double bx0 = 0, by0 = 0, bx1 = 0, by1 = 0;
@@ -2417,6 +2429,7 @@ struct vp_ctx {
   // far field on its own stream and host thread when it overlaps the near and
   // self stages (FMM); fs is the stream the far-path functions use
   cudaStream_t s2 = nullptr, fs = nullptr;
+  cudaStream_t s3 = nullptr, ss = nullptr;  // self + point-sum stream (ss: where launch_self goes)
   std::mutex err_mu;
   DevBuf f_tmp;
   int far_launches = 0;
@@ -2795,7 +2808,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, 2 * sizeof(unsigned), c->stream));
   LeafOut lo{c->d_lcntc.as<int64_t>(), c->d_lcntd.as<int64_t>(), c->d_loffc.as<int64_t>(), c->d_loffd.as<int64_t>(),
-             nullptr, nullptr, c->d_ldeep.as<int32_t>(), c->d_nover.as<unsigned>() + 1, c->cache_depth};
+             nullptr, nullptr, c->d_ldeep.as<int32_t>(), c->d_nover.as<unsigned>() + 1, c->cache_depth, pelem};
   k_near_leaves<false><<<nblk(n, 4 * kLeafChunk), 128, 0, c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), lo,
       c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
@@ -2855,13 +2868,13 @@ template <int P>
 void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
                  double* corr, double* sub, int64_t* panels) {
   const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
-  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->stream>>>(
+  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->ss>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
       c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
       sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c));
   if (has_curves(c)) {
     const int cb = (int)std::min<int64_t>(nblk(n, CURV_WARPS), (int64_t)c->sm_count * 16);
-    k_self_curved<P><<<std::max(cb, 1), CURV_WARPS * 32, 0, c->stream>>>(
+    k_self_curved<P><<<std::max(cb, 1), CURV_WARPS * 32, 0, c->ss>>>(
         n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), curves_dev(c), c->d_sx.as<double>(),
         c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), corr, sub, panels,
         c->d_stats.as<unsigned long long>());
@@ -3426,6 +3439,30 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false)) return rc;
     CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
   }
+  // Pair stage.  The self pairs and the per-target point sums need only the
+  // lists and the sources, so they run on s3 beside the near chain (whose
+  // leaf walk is latency-bound and whose host syncs would otherwise leave
+  // the GPU idle); the main stream has the higher priority, so the near
+  // chain's blocks go first and K5 fills the rest.
+  CUDA_TRY(c, c->d_corr_self.ensure(sizeof(double) * (T + 1)));
+  CUDA_TRY(c, c->d_psum.ensure(sizeof(double) * (T + 1)));
+  const cudaEvent_t fork = overlap ? ev[6] : ev[2];
+  struct SelfStream {  // launch_self goes to s3 until this scope ends
+    vp_ctx* c;
+    ~SelfStream() { c->ss = c->stream; }
+  } self_stream{c};
+  CUDA_TRY(c, cudaStreamWaitEvent(c->s3, fork, 0));
+  c->ss = c->s3;
+  VP_DISPATCH_P(c->p, launch_self, c, T, nullptr, c->d_self.as<int32_t>(), txy, c->d_corr_self.as<double>(),
+                nullptr, nullptr);
+  CUDA_TRY(c, cudaEventRecord(ev[9], c->s3));
+  k_psum_tgt<<<(unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64), PT_WARPS * 32, 0,
+               c->s3>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
+                        c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
+                        c->d_psum.as<double>());
+  CUDA_TRY(c, cudaEventRecord(ev[8], c->s3));
+  c->ss = c->stream;
+  c->last_launches += 2;
   CUDA_TRY(c, c->d_ptgt.ensure(sizeof(int32_t) * (n_ids + 1)));
   CUDA_TRY(c, c->d_corr.ensure(sizeof(double) * (n_ids + 1)));
   if (n_ids > 0) {
@@ -3435,27 +3472,19 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
                              c->d_corr.as<double>(), nullptr, nullptr, T, c->d_off.as<int64_t>())) return rc;
   }
   CUDA_TRY(c, cudaEventRecord(ev[3], c->stream));
-  CUDA_TRY(c, c->d_corr_self.ensure(sizeof(double) * (T + 1)));
-  VP_DISPATCH_P(c->p, launch_self, c, T, nullptr, c->d_self.as<int32_t>(), txy, c->d_corr_self.as<double>(),
-                nullptr, nullptr);
-  c->last_launches += 1;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[8], 0));
   CUDA_TRY(c, cudaEventRecord(ev[4], c->stream));
   if (far_thread.joinable()) far_thread.join();
   c->fs = c->stream;
   if (far_rc) return far_rc;
   c->last_launches += c->far_launches;
   if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, ev[2], 0));
-  CUDA_TRY(c, c->d_psum.ensure(sizeof(double) * (T + 1)));
-  k_psum_tgt<<<(unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64), PT_WARPS * 32, 0,
-               c->stream>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
-                            c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-                            c->d_psum.as<double>());
   CUDA_TRY(c, c->d_neart.ensure(sizeof(double) * (T + 1)));
   k_assemble<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_ufar.as<double>(), c->d_psum.as<double>(),
                                                    c->d_neart.as<double>(), c->d_off.as<int64_t>(),
                                                    c->d_corr.as<double>(), c->d_corr_self.as<double>(), u);
   k_count_self<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_self.as<int32_t>(), c->d_stats.as<unsigned long long>());
-  c->last_launches += 3;
+  c->last_launches += 2;
   CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
   CUDA_TRY(c, cudaGetLastError());
   unsigned long long hs[8];
@@ -3482,8 +3511,8 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     st->far_method = c->far_method;
     st->fmm_levels = c->far_method == 1 ? c->fmm_levels : 0;
     st->fmm_outside = c->far_method == 1 ? c->fmm_outside : 0;
-    float ms[5];
-    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+    float ms[2];
+    for (int i = 0; i < 2; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
     st->t_list_ms = ms[0];
     float msrc = 0, mfar = 0;
     cudaEventElapsedTime(&msrc, ev[1], ev[6]);
@@ -3491,10 +3520,13 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     st->t_sources_ms = msrc;
     st->t_far_kernel_ms = mfar;
     st->t_far_ms = ms[1];
-    float mnear = ms[2];
-    if (overlap) cudaEventElapsedTime(&mnear, ev[6], ev[3]);  // near starts with the far field
+    float mnear = 0, mself = 0, mpair = 0;
+    cudaEventElapsedTime(&mnear, fork, ev[3]);  // with the FMM, near starts beside the far field
+    cudaEventElapsedTime(&mself, fork, ev[9]);  // K5 on s3, beside the near chain
+    cudaEventElapsedTime(&mpair, fork, ev[4]);  // near + self + point sums, overlapped
     st->t_near_ms = mnear;
-    st->t_self_ms = ms[3];
+    st->t_self_ms = mself;
+    st->t_pair_ms = mpair;
     float tot = 0;
     cudaEventElapsedTime(&tot, ev[0], ev[5]);
     st->t_total_ms = tot;
@@ -3526,12 +3558,18 @@ int vp_create(int device, vp_ctx** out) {
   vp_ctx* c = new vp_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess) {
+  // the main stream (lists, near chain) outranks s2 (FMM far) and s3 (self,
+  // point sums), which fill the SMs the near chain leaves free
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (std::getenv("VP_FLAT_PRIO")) prio_hi = prio_lo;
+  if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return 3;
   }
-  c->fs = c->stream;
+  c->fs = c->ss = c->stream;
   for (auto& e : c->ev) cudaEventCreate(&e);
   double cn[kMaxModes];
   for (int n2 = 0; n2 <= kMaxPdev; ++n2)
@@ -3620,6 +3658,7 @@ void vp_destroy(vp_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->s2) cudaStreamDestroy(c->s2);
+  if (c->s3) cudaStreamDestroy(c->s3);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
