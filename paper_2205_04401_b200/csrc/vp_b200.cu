@@ -1436,7 +1436,7 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
 // rows past a batch and the same fixed summation order per target.
 template <int K8>
 __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
-    k_near_c8(int64_t T, const int64_t* __restrict__ toff, const int32_t* __restrict__ pair_elem,
+    k_near_c8(int64_t T, const int64_t* __restrict__ tl, const int32_t* __restrict__ pair_elem,
               const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
               const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
               const double* __restrict__ gcache, const double* __restrict__ zrow,
@@ -1464,15 +1464,15 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
   }
   __syncthreads();
   const unsigned laneoff = 16u * (threadIdx.x & (kLogCopies - 1));
+  // Targets in grid-stride order; target t's cached leaves are
+  // [tl[t], tl[t + 1]) (tl[t] = loff[toff[t]], one load deep), and the codes
+  // of the next batch are loaded while the current batch computes.
   for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
-    const int64_t q0 = toff[t], q1 = toff[t + 1];
+    const int64_t L0 = tl[t], L1 = tl[t + 1];
     double acc = 0.0, acc1 = 0.0;
-    if (q1 > q0) {
-      const int64_t L0 = loff[q0], L1 = loff[q1];
+    if (L1 > L0) {
       const double2 tp = txy[t];
       const double tx = tp.x, ty = tp.y;
-      // the leaf codes carry their element (tag_cached); the next batch's
-      // codes are loaded while this batch computes
       unsigned long long code_n = lane < L1 - L0 ? leaves[L0 + lane] : 0ull;
       for (int64_t lb = L0; lb < L1; lb += 32) {
         const int nb = (int)min((int64_t)32, L1 - lb);
@@ -1516,12 +1516,14 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
           }
 #pragma unroll
           for (int k = 0; k < K8; ++k) {
-            if (k + 1 < K8 || nok[k]) {
-              const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
-              const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
-              double& a = (k & 1) ? acc1 : acc;  // two chains: K8 DFMAs deep -> K8 / 2
-              a = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), a);
-            }
+            // no branch for the last slot's missing nodes (49 = 6 x 8 + 1):
+            // there nu = nv = 0 and g = 0, the log of |D0|^2 is finite (also
+            // for zero rows: the bit-level log maps 0 to a finite value), so
+            // the slot adds exactly 0 and the warp does not diverge
+            const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
+            const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
+            double& a = (k & 1) ? acc1 : acc;  // two chains: K8 DFMAs deep -> K8 / 2
+            a = fma(g[k], far_log_r2<false, true>(tab, laneoff, c3ff, fma(dx, dx, dy * dy)), a);
           }
         }
       }
@@ -1529,6 +1531,14 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
     const double val = warp_sum(acc + acc1);
     if (lane == 0) part_t[t] = val;
   }
+}
+
+// tl[t] = loff[toff[t]], t in [0, T]: target t's cached leaves are
+// [tl[t], tl[t + 1]) (k_near_c8 reads its ranges one load deep)
+__global__ void k_tgt_leafrange(int64_t T, const int64_t* __restrict__ toff, const int64_t* __restrict__ loff,
+                                int64_t* __restrict__ tl) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= T) tl[t] = loff[toff[t]];
 }
 
 // Point sums of subtract-and-add for the per-pair API: part_s[p] =
@@ -2417,6 +2427,7 @@ struct vp_ctx {
   int64_t cache_max_bytes = 12ll << 30;
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
   DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
+  DevBuf d_tl;  // per-target cached-leaf ranges (k_tgt_leafrange)
   DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
   DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
   int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
@@ -2693,8 +2704,10 @@ template <int K8>
 void launch_near_c8(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
                     const double* gc) {
   const int blocks = (int)std::min<int64_t>(nblk(T, NG_WARPS), (int64_t)c->sm_count * 24);
+  k_tgt_leafrange<<<nblk(T + 1, 256), 256, 0, c->stream>>>(T, toff, c->d_loffc.as<int64_t>(), c->d_tl.as<int64_t>());
+  c->last_launches += 1;
   k_near_c8<K8><<<std::max(blocks, 1), NG_WARPS * 32, sizeof(LogTab), c->stream>>>(
-      T, toff, pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
+      T, c->d_tl.as<int64_t>(), pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
       c->d_rules.as<RulesDev>(), gc, gc + c->n_tri * (int64_t)(((1ll << (2 * (c->cache_depth + 1))) - 1) / 3) *
       c->rules.len_n, c->d_slotref.as<double>(), c->cache_depth, c->d_neart.as<double>(), 0x3ff00000u);
 }
@@ -2849,6 +2862,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
   if (toff) {
     CUDA_TRY(c, c->d_neart.ensure(sizeof(double) * (T + 1)));
+    CUDA_TRY(c, c->d_tl.ensure(sizeof(int64_t) * (T + 1)));
     if (c->cache_depth < 0) CUDA_TRY(c, cudaMemsetAsync(c->d_neart.p, 0, sizeof(double) * T, c->stream));
   }
   VP_DISPATCH_P(c->p, launch_near_int, c, n, ptgt, pelem, txy, corr, sub, (int64_t)ndeep, T, toff);
