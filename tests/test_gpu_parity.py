@@ -92,6 +92,24 @@ def test_u_config2_sample(cfg2):
     assert rel(u_g[sub], u_o) <= REL_TOL
 
 
+@pytest.mark.parametrize("far", ["direct", "fmm"])
+def test_pair_stage_streams(cfg2, far):
+    """Self pairs and point sums run on their own stream beside the near chain:
+    the stage's wall time covers both and u does not depend on the far method
+    beyond rounding (and is bit-identical run to run)."""
+    pr, ev, _ = cfg2
+    ev.set_far_method(far)
+    try:
+        u1, st = ev.evaluate(pr.txy)
+        u2, _ = ev.evaluate(pr.txy)
+    finally:
+        ev.set_far_method("direct")
+    assert np.array_equal(u1, u2)
+    assert st["t_pair_ms"] > 0.0
+    assert st["t_pair_ms"] >= max(st["t_near_ms"], st["t_self_ms"]) - 1e-3
+    assert st["t_total_ms"] >= st["t_pair_ms"]
+
+
 def test_near_pairs_per_pair(cfg2):
     pr, ev, O = cfg2
     s, off, ids = O.nearlist(pr.txy[::101])
