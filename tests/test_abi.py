@@ -105,3 +105,27 @@ def test_density_projection_reproduces_polynomials():
         y = vxy[0] + xi * (vxy[1] - vxy[0]) + eta * (vxy[2] - vxy[0])
         f = co[0] @ ob.koornwinder(1, xi, eta)
         assert abs(f - (0.5 + 2.0 * y[0] - 1.0 * y[1])) < 1e-14
+
+
+def header_struct_fields(header, typedef_name):
+    """Field names, in order, of `typedef struct { ... } typedef_name;` in include/."""
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    m = re.search(r"typedef struct\s*\{([^}]*)\}\s*" + typedef_name + r"\s*;", src)
+    assert m, f"{typedef_name} not found in {header}"
+    names = []
+    for decl in m.group(1).split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        for part in decl.split(","):  # "double a, b" style declarations
+            names.append(re.sub(r"\[.*\]", "", part).strip().split()[-1].lstrip("*"))
+    return names
+
+
+@pytest.mark.parametrize("header,name,cls", [("vp.h", "vp_stats", "VpStats"), ("vp.h", "vp_rules", "VpRules")])
+def test_ctypes_structs_mirror_headers(header, name, cls):
+    """The ctypes mirrors of the C-ABI structs list the header's fields in the
+    header's order (a field added on one side only shifts every later one)."""
+    fields = [f for f, _ in getattr(_lib, cls)._fields_]
+    assert fields == header_struct_fields(header, name)
