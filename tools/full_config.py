@@ -41,7 +41,7 @@ if a.check > 0:
 out = {"config": a.config, "q": pr.q, "far": a.far, "n_tri": pr.n_tri, "targets": pr.n_tgt,
        "sources": st["n_sources"], "near_pairs": st["n_near_pairs"], "leaves": st["n_leaves"],
        "panels": st["n_panels"], "outside": st["n_outside"], "fmm_levels": st["fmm_levels"],
-       "device_ms": {k: st[k] for k in ("t_list_ms", "t_sources_ms", "t_far_ms", "t_near_ms", "t_self_ms", "t_total_ms")},
+       "device_ms": {k: st[k] for k in ("t_list_ms", "t_sources_ms", "t_far_ms", "t_near_ms", "t_self_ms", "t_pair_ms", "t_total_ms")},
        "wall_s": wall, "targets_per_s_device": pr.n_tgt / (st["t_total_ms"] * 1e-3),
        "parity_sample": a.check, "u_rel_err_vs_oracle": err, "oracle_cpu_s": ocpu,
        "oracle_targets_per_s_cpu": (a.check / ocpu) if a.check > 0 else None, "generate_s": gen}
