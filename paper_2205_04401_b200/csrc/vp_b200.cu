@@ -1809,10 +1809,20 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     for (int o = lane; o < 3 * 2 * NP; o += 32) {
       const int k = o >= 4 * NP ? 2 : (o >= 2 * NP ? 1 : 0), oo = o - k * 2 * NP;
       const double* Fk = F + k * M;
-      double sum = 0.0;
-#pragma unroll 4
-      for (int q = 0; q < M; ++q) sum = fma(sT2[oo * M + q], Fk[q], sum);
-      sE[wid][k][oo] = sum;
+      const double* Tk = sT2 + oo * M;
+      // four independent DFMA chains: one chain of M dependent DFMAs was the
+      // kernel's top stall (ncu source page)
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int q = 0;
+#pragma unroll 2
+      for (; q + 4 <= M; q += 4) {
+        s0 = fma(Tk[q], Fk[q], s0);
+        s1 = fma(Tk[q + 1], Fk[q + 1], s1);
+        s2 = fma(Tk[q + 2], Fk[q + 2], s2);
+        s3 = fma(Tk[q + 3], Fk[q + 3], s3);
+      }
+      for (; q < M; ++q) s0 = fma(Tk[q], Fk[q], s0);
+      sE[wid][k][oo] = (s0 + s1) + (s2 + s3);
     }
     __syncwarp();
     double acc = 0.0;
