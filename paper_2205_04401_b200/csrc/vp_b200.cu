@@ -952,7 +952,7 @@ __device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __
     xi[i] = fma(nxy[i].y, ca[i].x, fma(nxy[i].x, ba[i].x, a[i].x));
     eta[i] = fma(nxy[i].y, ca[i].y, fma(nxy[i].x, ba[i].y, a[i].y));
   }
-  density_n<P, NPT>(cc, xi, eta, f);
+  density_n<P, NPT, true>(cc, xi, eta, f);
   double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < NPT; ++i) {

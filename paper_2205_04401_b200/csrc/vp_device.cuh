@@ -103,6 +103,31 @@ __host__ __device__ constexpr double kc_jc(int m, int k) {
   return 2.0 * (k + (2 * m + 1)) * k * (2.0 * k + (2 * m + 1) + 2) / kc_c1(m, k);
 }
 
+// The same coefficients as a __constant__ table (density_n<.., CT = true>),
+// loaded by LDC/LDCU: as 64-bit immediates the compiler rebuilt each one
+// with a UMOV pair per use (17 % of k_near_int's instructions; 0.98 ->
+// 0.95 ms).  K5 keeps the immediates (with the table it spilled more and
+// ran 4 % slower).
+constexpr int kKcN = 13;  // p <= 12
+struct KcTable {
+  double ja[kKcN * kKcN], jb[kKcN * kKcN], jc[kKcN * kKcN], la[kKcN], lb[kKcN];
+};
+__host__ __device__ constexpr KcTable make_kc_table() {
+  KcTable t{};
+  for (int m = 0; m < kKcN; ++m) {
+    const double a = 2 * m + 1;
+    t.la[m] = m >= 1 ? kc_la(m) : 1.0;
+    t.lb[m] = m >= 1 ? kc_lb(m) : 0.0;
+    for (int k = 0; k < kKcN; ++k) {
+      t.ja[m * kKcN + k] = k == 0 ? 0.5 * (a + 2.0) : kc_ja(m, k);
+      t.jb[m * kKcN + k] = k == 0 ? 0.5 * a : kc_jb(m, k);
+      t.jc[m * kKcN + k] = k == 0 ? 0.0 : kc_jc(m, k);
+    }
+  }
+  return t;
+}
+__constant__ KcTable c_kc = make_kc_table();
+
 // f(x, y) = sum_j cc_j K_j(x, y) where cc_j already includes the
 // normalisation c_mn (pre-scaled per element).  Template recursion over
 // (m, k) makes every recurrence coefficient a compile-time constant (no
@@ -131,7 +156,7 @@ struct Pts {
   double v[NPT];
 };
 
-template <int P, int m, int k, int NPT, class CC>
+template <int P, int m, int k, int NPT, bool CT, class CC>
 __device__ __forceinline__ void clenshaw_m(const CC& cc, const Pts<NPT>& t, Pts<NPT>& b1, Pts<NPT>& b2) {
   // processes k = P - m down to 0 for fixed m; on exit b1 = b_0 = S_m
   if constexpr (k >= 0) {
@@ -144,9 +169,9 @@ __device__ __forceinline__ void clenshaw_m(const CC& cc, const Pts<NPT>& t, Pts<
       }
     } else {
       constexpr double a = 2 * m + 1;
-      constexpr double ja = (k == 0) ? 0.5 * (a + 2.0) : kc_ja(m, k);
-      constexpr double jb = (k == 0) ? 0.5 * a : kc_jb(m, k);
-      constexpr double jc1 = kc_jc(m, k + 1);  // beta_{k+1}
+      const double ja = CT ? c_kc.ja[m * kKcN + k] : ((k == 0) ? 0.5 * (a + 2.0) : kc_ja(m, k));
+      const double jb = CT ? c_kc.jb[m * kKcN + k] : ((k == 0) ? 0.5 * a : kc_jb(m, k));
+      const double jc1 = CT ? c_kc.jc[m * kKcN + k + 1] : kc_jc(m, k + 1);  // beta_{k+1}
 #pragma unroll
       for (int i = 0; i < NPT; ++i) {
         const double al = fma(ja, t.v[i], jb);
@@ -156,17 +181,17 @@ __device__ __forceinline__ void clenshaw_m(const CC& cc, const Pts<NPT>& t, Pts<
         b1.v[i] = bk;
       }
     }
-    clenshaw_m<P, m, k - 1, NPT, CC>(cc, t, b1, b2);
+    clenshaw_m<P, m, k - 1, NPT, CT, CC>(cc, t, b1, b2);
   }
 }
 
-template <int P, int m, int NPT, class CC>
+template <int P, int m, int NPT, bool CT, class CC>
 __device__ __forceinline__ void koorn_modes_n(const CC& cc, const Pts<NPT>& t, const Pts<NPT>& u,
                                               const Pts<NPT>& v2, Pts<NPT>& Lm, Pts<NPT>& Lprev,
                                               Pts<NPT>& f) {
   if constexpr (m <= P) {
     Pts<NPT> b1, b2;
-    clenshaw_m<P, m, P - m, NPT, CC>(cc, t, b1, b2);
+    clenshaw_m<P, m, P - m, NPT, CT, CC>(cc, t, b1, b2);
 #pragma unroll
     for (int i = 0; i < NPT; ++i) f.v[i] = fma(b1.v[i], Lm.v[i], f.v[i]);
     if constexpr (m < P) {
@@ -176,19 +201,19 @@ __device__ __forceinline__ void koorn_modes_n(const CC& cc, const Pts<NPT>& t, c
         if constexpr (m == 0) {
           Ln = u.v[i];
         } else {
-          constexpr double la = kc_la(m), lb = kc_lb(m);
+          const double la = CT ? c_kc.la[m] : kc_la(m), lb = CT ? c_kc.lb[m] : kc_lb(m);
           Ln = fma(la * u.v[i], Lm.v[i], -lb * v2.v[i] * Lprev.v[i]);
         }
         Lprev.v[i] = Lm.v[i];
         Lm.v[i] = Ln;
       }
-      koorn_modes_n<P, m + 1, NPT, CC>(cc, t, u, v2, Lm, Lprev, f);
+      koorn_modes_n<P, m + 1, NPT, CT, CC>(cc, t, u, v2, Lm, Lprev, f);
     }
   }
 }
 
-// f at NPT points (x[i], y[i])
-template <int P, int NPT, class CC>
+// f at NPT points (x[i], y[i]); CT: recurrence constants from c_kc
+template <int P, int NPT, bool CT = false, class CC>
 __device__ __forceinline__ void density_n(const CC& cc, const double* x, const double* y, double* out) {
   Pts<NPT> t, u, v2, Lm, Lprev, f;
 #pragma unroll
@@ -201,7 +226,7 @@ __device__ __forceinline__ void density_n(const CC& cc, const double* x, const d
     Lprev.v[i] = 0.0;
     f.v[i] = 0.0;
   }
-  koorn_modes_n<P, 0, NPT, CC>(cc, t, u, v2, Lm, Lprev, f);
+  koorn_modes_n<P, 0, NPT, CT, CC>(cc, t, u, v2, Lm, Lprev, f);
 #pragma unroll
   for (int i = 0; i < NPT; ++i) out[i] = f.v[i];
 }
@@ -209,7 +234,7 @@ __device__ __forceinline__ void density_n(const CC& cc, const double* x, const d
 template <int P, class CC>
 __device__ __forceinline__ double density(const CC& cc, double x, double y) {
   double o;
-  density_n<P, 1, CC>(cc, &x, &y, &o);
+  density_n<P, 1, false, CC>(cc, &x, &y, &o);
   return o;
 }
 
