@@ -3588,7 +3588,8 @@ int vp_create(int device, vp_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (std::getenv("VP_FLAT_PRIO")) prio_hi = prio_lo;
   if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->s2, cudaStreamNonBlocking,
+                                   std::getenv("VP_S2_HIGH") ? prio_hi : prio_lo) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return 3;
