@@ -53,6 +53,15 @@ class VpoStats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
 
 
+class VpoConfigInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_vert", ctypes.c_int64), ("n_tri", ctypes.c_int64), ("n_tgt", ctypes.c_int64),
+        ("p", ctypes.c_int), ("q", ctypes.c_int), ("density_kind", ctypes.c_int), ("n_params", ctypes.c_int),
+        ("params", ctypes.c_double * 64), ("eps", ctypes.c_double), ("seed", ctypes.c_uint64),
+        ("staggered", ctypes.c_int), ("pad", ctypes.c_int),
+    ]
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
@@ -84,6 +93,18 @@ def lib():
             "vpo_near_pair": (i32, [P, dbl, dbl, ctypes.c_int32, _d_p, _d_p, _i64_p, ctypes.POINTER(ctypes.c_int32)]),
             "vpo_self": (i32, [P, dbl, dbl, ctypes.c_int32, _d_p, _d_p, _i64_p]),
             "vpo_evaluate": (i32, [P, i64, _d_p, i32, _d_p, _d_p, ctypes.POINTER(VpoStats)]),
+            "vpo_open": (i32, [P, ctypes.POINTER(ctypes.c_void_p)]),
+            "vpo_ctx_evaluate": (i32, [vp_, i64, _d_p, i32, _d_p, _d_p, ctypes.POINTER(VpoStats)]),
+            "vpo_close": (None, [vp_]),
+            "vpo_inputs_last_error": (ctypes.c_char_p, []),
+            "vpo_lattice_nodes": (i32, [i32, _d_p, _d_p]),
+            "vpo_gauss_jacobi10": (i32, [i32, _d_p, _d_p]),
+            "vpo_simplex_rule": (i32, [i32, ctypes.POINTER(i32), _d_p, _d_p, _d_p]),
+            "vpo_ggq": (i32, [i32, _d_p, _d_p, ctypes.POINTER(dbl)]),
+            "vpo_density_eval": (dbl, [i32, _d_p, i32, dbl, dbl]),
+            "vpo_project_density": (i32, [i64, _d_p, i64, _i32_p, i32, i32, _d_p, i32, _d_p]),
+            "vpo_config_info_get": (i32, [i32, i32, ctypes.c_uint64, ctypes.POINTER(VpoConfigInfo)]),
+            "vpo_config_fill": (i32, [i32, i32, ctypes.c_uint64, _d_p, _i32_p, _d_p, _d_p]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)
@@ -148,6 +169,10 @@ class Oracle:
     @classmethod
     def from_problem(cls, pr, near_model=0, ball_factor=1.5):
         return cls(pr.vxy, pr.tri, pr.p, pr.coeffs, pr.rules, near_model, ball_factor)
+
+    def open(self):
+        """Persistent context (setup once, evaluate many target batches)."""
+        return OracleCtx(self)
 
     def nearlist(self, txy):
         t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)
@@ -277,3 +302,119 @@ def ref_arclength(kind, params, s):
     if rc != 0:
         raise OracleError(rc, "reference reparametrize failed")
     return xy, tg, dd, ln.value, bool(ccw.value)
+
+
+class OracleCtx:
+    """vpo_open / vpo_ctx_evaluate / vpo_close: the oracle's setup (element
+    models, quadtree, sources) done once for many evaluations."""
+
+    def __init__(self, oracle):
+        self.o = oracle  # keeps the problem arrays alive
+        h = ctypes.c_void_p()
+        _check(lib().vpo_open(ctypes.byref(oracle.pr), ctypes.byref(h)))
+        self.h = h
+
+    def evaluate(self, txy, nthreads=0):
+        t = np.ascontiguousarray(txy, dtype=np.float64).reshape(-1, 2)
+        u, uf = np.zeros(t.shape[0]), np.zeros(t.shape[0])
+        st = VpoStats()
+        _check(lib().vpo_ctx_evaluate(self.h, t.shape[0], _d(t), nthreads, _d(u), _d(uf), ctypes.byref(st)))
+        return u, uf, st.as_dict()
+
+    def close(self):
+        if self.h:
+            lib().vpo_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# the oracle's own inputs (vp_oracle_inputs.cpp): rules, configurations and
+# density coefficients generated without the product library
+
+def _check_in(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().vpo_inputs_last_error().decode())
+
+
+def simplex_rule(order):
+    n = ctypes.c_int()
+    _check_in(lib().vpo_simplex_rule(order, ctypes.byref(n), None, None, None))
+    x, y, w = (np.zeros(n.value) for _ in range(3))
+    _check_in(lib().vpo_simplex_rule(order, ctypes.byref(n), _d(x), _d(y), _d(w)))
+    return x, y, w
+
+
+def gauss_jacobi10(n):
+    x, w = np.zeros(n), np.zeros(n)
+    _check_in(lib().vpo_gauss_jacobi10(n, _d(x), _d(w)))
+    return x, w
+
+
+def ggq(ng):
+    r, w, res = np.zeros(ng + 1), np.zeros(ng + 1), ctypes.c_double()
+    _check_in(lib().vpo_ggq(ng, _d(r), _d(w), ctypes.byref(res)))
+    return r, w, res.value
+
+
+def lattice_nodes(p):
+    m = (p + 1) * (p + 2) // 2
+    x, y = np.zeros(m), np.zeros(m)
+    _check_in(lib().vpo_lattice_nodes(p, _d(x), _d(y)))
+    return x, y
+
+
+def project_density(vxy, tri, p, kind, params=()):
+    vxy = np.ascontiguousarray(vxy, dtype=np.float64).reshape(-1, 2)
+    tri = np.ascontiguousarray(tri, dtype=np.int32).reshape(-1, 3)
+    prm = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(-1))
+    out = np.zeros((tri.shape[0], (p + 1) * (p + 2) // 2))
+    _check_in(lib().vpo_project_density(vxy.shape[0], _d(vxy), tri.shape[0], tri.ctypes.data_as(_i32_p), p, kind,
+                                        _d(prm) if prm.size else None, prm.size, _d(out)))
+    return out
+
+
+class OracleRules:
+    """Rules in the shape Oracle expects (far, near, gl, ggq tuples), built by
+    the oracle's own generators; defaults mirror SPEC.md:733."""
+
+    def __init__(self, q, n_n=12, n_l=16, n_g=8, eps=1e-12):
+        self.q, self.n_n, self.n_g, self.eps = q, n_n, n_g, eps
+        self.far = simplex_rule(q)
+        self.near = simplex_rule(n_n)
+        self.gl = gauss_legendre(n_l)
+        r, w, _ = ggq(n_g)
+        self.ggq = (r, w)
+
+
+class OracleProblem:
+    """One BASELINE config from the oracle's own seeded generators."""
+
+    def __init__(self, config, q_override=0, seed=0):
+        info = VpoConfigInfo()
+        _check_in(lib().vpo_config_info_get(config, q_override, seed, ctypes.byref(info)))
+        self.config, self.seed = config, seed
+        self.p, self.q, self.eps = info.p, info.q, info.eps
+        self.density_kind = info.density_kind
+        self.params = np.array(info.params[:info.n_params])
+        self.staggered = bool(info.staggered)
+        self.vxy = np.zeros((info.n_vert, 2))
+        self.tri = np.zeros((info.n_tri, 3), dtype=np.int32)
+        self.txy = np.zeros((info.n_tgt, 2))
+        self.coeffs = np.zeros((info.n_tri, (self.p + 1) * (self.p + 2) // 2))
+        _check_in(lib().vpo_config_fill(config, q_override, seed, _d(self.vxy), self.tri.ctypes.data_as(_i32_p),
+                                        _d(self.txy), _d(self.coeffs)))
+        self.rules = OracleRules(self.q, eps=self.eps)
+
+    @property
+    def n_tri(self):
+        return self.tri.shape[0]
+
+    @property
+    def n_tgt(self):
+        return self.txy.shape[0]

@@ -572,6 +572,7 @@ struct Setup {
       if (p->len_q <= 0) return fail(1, "oracle: empty far rule");
       const int L = p->len_q;
       sx.resize(E * L); sy.resize(E * L); sq.resize(E * L);
+#pragma omp parallel for schedule(static)
       for (int64_t e = 0; e < E; ++e) {
         const double* c = p->coeffs + e * M;
         for (int i = 0; i < L; ++i) {
@@ -1007,6 +1008,7 @@ double vpo_w_edge(int len, const double* x, const double* y, const double* w) {
 // rules.hpp:60-85
 int vpo_validate_rule(int order, int len, const double* x, const double* y, const double* w) {
   if (len <= 0) return fail(2, "rule table: empty rule");
+  if (order < 0 || order > kMaxOrder) return fail(1, "rule table: order out of range (invariant: 0 <= order <= 32)");
   double ws = 0.0;
   for (int i = 0; i < len; ++i) {
     if (w[i] <= 0.0) return fail(2, "rule table: non-positive weight (invariant: weights > 0)");
@@ -1133,29 +1135,47 @@ int vpo_sources(const vpo_problem* pr, double* sx, double* sy, double* q) {
   return 0;
 }
 
+// Neumaier-compensated direct sum (fmm_eval direct path, SPEC.md:572-580,
+// :618).  Targets go four at a time through one sweep of the sources (each
+// target keeps its own sum in source order, so the bits are those of the
+// one-target loop); the sweep is what costs memory bandwidth on the host.
+static inline void neumaier(double& sum, double& comp, double term) {
+  const double tt = sum + term;
+  if (std::abs(sum) >= std::abs(term))
+    comp += (sum - tt) + term;
+  else
+    comp += (term - tt) + sum;
+  sum = tt;
+}
+
 static void far_sum_impl(const Setup& s, int64_t n_tgt, const double* txy, double* u_far) {
   const int64_t S = (int64_t)s.sx.size();
   const double* sx = s.sx.data();
   const double* sy = s.sy.data();
   const double* sq = s.sq.data();
-#pragma omp for schedule(static)
-  for (int64_t t = 0; t < n_tgt; ++t) {
-    const double tx = txy[2 * t], ty = txy[2 * t + 1];
-    // Neumaier-compensated sum (fmm_eval direct path)
-    double sum = 0.0, comp = 0.0;
-    for (int64_t j = 0; j < S; ++j) {
-      const double dx = tx - sx[j], dy = ty - sy[j];
-      const double r2 = dx * dx + dy * dy;
-      if (!(r2 > 0.0)) continue;  // coincident pair contributes 0
-      const double term = sq[j] * std::log(r2);
-      const double tt = sum + term;
-      if (std::abs(sum) >= std::abs(term))
-        comp += (sum - tt) + term;
-      else
-        comp += (term - tt) + sum;
-      sum = tt;
+  constexpr int B = 4;
+  const int64_t nb = (n_tgt + B - 1) / B;
+#pragma omp for schedule(dynamic, 1)
+  for (int64_t blk = 0; blk < nb; ++blk) {
+    const int64_t t0 = blk * B;
+    const int nt = (int)std::min<int64_t>(B, n_tgt - t0);
+    double tx[B], ty[B], sum[B], comp[B];
+    for (int k = 0; k < B; ++k) {
+      const int64_t t = t0 + std::min(k, nt - 1);
+      tx[k] = txy[2 * t];
+      ty[k] = txy[2 * t + 1];
+      sum[k] = comp[k] = 0.0;
     }
-    u_far[t] = sum + comp;
+    for (int64_t j = 0; j < S; ++j) {
+      const double xj = sx[j], yj = sy[j], qj = sq[j];
+      for (int k = 0; k < B; ++k) {
+        const double dx = tx[k] - xj, dy = ty[k] - yj;
+        const double r2 = dx * dx + dy * dy;
+        if (!(r2 > 0.0)) continue;  // coincident pair contributes 0
+        neumaier(sum[k], comp[k], qj * std::log(r2));
+      }
+    }
+    for (int k = 0; k < nt; ++k) u_far[t0 + k] = sum[k] + comp[k];
   }
 }
 
@@ -1202,11 +1222,10 @@ int vpo_self(const vpo_problem* pr, double tx, double ty, int32_t elem, double* 
   return 0;
 }
 
-int vpo_evaluate(const vpo_problem* pr, int64_t n_tgt, const double* txy, int nthreads,
-                 double* u, double* u_far, vpo_stats* st) {
+static int evaluate_setup(const Setup& s, int64_t n_tgt, const double* txy, int nthreads, double* u,
+                          double* u_far, vpo_stats* st) {
+  const vpo_problem* pr = s.pr;
   if (n_tgt < 0 || (n_tgt > 0 && (!txy || !u))) return fail(1, "evaluate: bad target array");
-  Setup s;
-  if (int rc = s.init(pr, true, true)) return rc;
   if (pr->n_l <= 0 || pr->n_g < 0 || !pr->gl_x || !pr->ggq_r) return fail(1, "evaluate: missing self rules");
   std::vector<double> uf(n_tgt);
   int64_t outside = 0, npairs = 0, nself = 0, leaves = 0, panels = 0, rle1 = 0, degen = 0;
@@ -1266,5 +1285,40 @@ int vpo_evaluate(const vpo_problem* pr, int64_t n_tgt, const double* txy, int nt
   }
   return 0;
 }
+
+int vpo_evaluate(const vpo_problem* pr, int64_t n_tgt, const double* txy, int nthreads,
+                 double* u, double* u_far, vpo_stats* st) {
+  Setup s;
+  if (int rc = s.init(pr, true, true)) return rc;
+  return evaluate_setup(s, n_tgt, txy, nthreads, u, u_far, st);
+}
+
+}  // extern "C"
+
+struct vpo_ctx {
+  Setup s;
+};
+
+extern "C" {
+
+int vpo_open(const vpo_problem* pr, vpo_ctx** out) {
+  if (!out) return fail(1, "open: null output");
+  *out = nullptr;
+  vpo_ctx* c = new vpo_ctx;
+  if (int rc = c->s.init(pr, true, true)) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+int vpo_ctx_evaluate(vpo_ctx* c, int64_t n_tgt, const double* txy, int nthreads, double* u, double* u_far,
+                     vpo_stats* st) {
+  if (!c) return fail(1, "evaluate: null context");
+  return evaluate_setup(c->s, n_tgt, txy, nthreads, u, u_far, st);
+}
+
+void vpo_close(vpo_ctx* c) { delete c; }
 
 }  // extern "C"

@@ -98,6 +98,43 @@ int vpo_evaluate(const vpo_problem* pr, int64_t n_tgt, const double* txy, int nt
                  double* u, double* u_far, vpo_stats* st);
 const char* vpo_last_error(void);
 
+/* Persistent oracle context: Setup::init once (element models, quadtree,
+ * sources), then any number of evaluations over target batches.  The
+ * problem's arrays must outlive the context. */
+typedef struct vpo_ctx vpo_ctx;
+int vpo_open(const vpo_problem* pr, vpo_ctx** out);
+int vpo_ctx_evaluate(vpo_ctx* ctx, int64_t n_tgt, const double* txy, int nthreads, double* u,
+                     double* u_far, vpo_stats* st);
+void vpo_close(vpo_ctx* ctx);
+
+/* ---- the oracle's own inputs (vp_oracle_inputs.cpp) ------------------- */
+typedef struct {
+  int64_t n_vert;
+  int64_t n_tri;
+  int64_t n_tgt;
+  int p;
+  int q;
+  int density_kind; /* 0 const, 1 sin3x cos2y + x^2, 2 gauss, 3 bumps, 4 cos4pix sin2piy, 5 linear */
+  int n_params;
+  double params[64];
+  double eps;
+  uint64_t seed;
+  int staggered;
+  int pad;
+} vpo_config_info;
+
+int vpo_lattice_nodes(int p, double* x, double* y);
+int vpo_gauss_jacobi10(int n, double* x, double* w);
+int vpo_simplex_rule(int order, int* len, double* x, double* y, double* w);
+int vpo_ggq(int ng, double* r, double* w, double* max_residual);
+double vpo_density_eval(int kind, const double* params, int n_params, double x, double y);
+int vpo_project_density(int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri, int p,
+                        int kind, const double* params, int n_params, double* coeffs);
+int vpo_config_info_get(int config, int q_override, uint64_t seed, vpo_config_info* info);
+int vpo_config_fill(int config, int q_override, uint64_t seed, double* vxy, int32_t* tri, double* txy,
+                    double* coeffs);
+const char* vpo_inputs_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif
