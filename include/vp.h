@@ -147,7 +147,10 @@ int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
 /* Far-field method: 0 = direct O(T S) sum (fmm_eval --direct, SPEC.md:618;
  * the default), 1 = 2-D Laplace FMM (fmm_eval; SURVEY.md
  * §8(f1)) with expansion order `order` (0 -> 31, 32 coefficients = one per lane) and about `leaf_size`
- * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity. */
+ * sources per leaf box (0 -> 40).  Both compute u_far to fp64 parity.
+ * 2 = none: vp_evaluate returns the corrections only, sum over N(t) and S(t)
+ * of (I_T(t) - point sum), for a caller that supplies its own far field
+ * (the subtract-and-add split of SPEC.md:612-615). */
 int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 
 /* Potential interpolation.  interp_coeffs (rules.hpp:

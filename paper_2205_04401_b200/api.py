@@ -506,8 +506,10 @@ class Evaluator:
         _check(self._L.vp_set_rules(self._h, ctypes.byref(self._rules_struct)), self._err())
 
     def set_far_method(self, method: str = "direct", order: int = 0, leaf_size: int = 0):
-        """'direct' (O(T S) sum, default) or 'fmm' (2-D Laplace FMM)."""
-        m = {"direct": 0, "fmm": 1}[method]
+        """'direct' (O(T S) sum, default), 'fmm' (2-D Laplace FMM)
+        or 'none' (evaluate returns the near/self corrections only, for a caller
+        that supplies its own far field: SPEC.md:612-615's subtract-and-add)."""
+        m = {"direct": 0, "fmm": 1, "none": 2}[method]
         _check(self._L.vp_set_far_method(self._h, m, order, leaf_size), self._err())
 
     def set_near_model(self, model: str = "precise", ball_factor: float = 1.5):

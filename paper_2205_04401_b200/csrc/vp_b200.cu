@@ -3223,26 +3223,35 @@ int far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_ch
 
 int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zero_check, DevBuf& part) {
   const int64_t S = c->n_tri * c->rules.len_q;
-  const int64_t tblocks = nblk(T, FAR_THREADS * FAR_R);
   // The source chunking depends on S only, never on T: every target's far
   // sum is the same fixed-order sum of chunk partials however the targets
-  // are batched or sharded (bitwise shard invariance).
-  int64_t chunk = std::max<int64_t>(4096, (S + 63) / 64);
+  // are batched or sharded (bitwise shard invariance).  Up to 256 chunks of
+  // >= 4096 sources: enough (target block, chunk) blocks that the last wave
+  // of one-block-per-SM launches is a small fraction (config 4 subset: 28 x
+  // 256 blocks = 48.4 waves of 148, against 12.1 waves with 64 chunks).
+  int64_t chunk = std::max<int64_t>(4096, (S + 255) / 256);
   chunk = (chunk + FAR_TILE - 1) / FAR_TILE * FAR_TILE;
   const int nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
-  CUDA_TRY(c, part.ensure(sizeof(double) * T * nsplit));
-  dim3 grid((unsigned)tblocks, (unsigned)nsplit);
-  if (zero_check)
-    k_far<true><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                          c->d_sq.as<double>(), chunk, part.as<double>(),
-                                                          0x3ff00000u);
-  else
-    k_far<false><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(T, txy, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                           c->d_sq.as<double>(), chunk, part.as<double>(),
-                                                           0x3ff00000u);
-  k_far_reduce<<<nblk(T, 256), 256, 0, c->fs>>>(T, nsplit, part.as<double>(), ufar);
+  // targets in batches so the [nsplit x batch] partials stay within 1 GiB
+  const int64_t tblk = (int64_t)FAR_THREADS * FAR_R;
+  const int64_t batch = std::max<int64_t>(tblk, ((1ll << 27) / nsplit) / tblk * tblk);
+  const int64_t Tb = std::min<int64_t>(T, batch);
+  CUDA_TRY(c, part.ensure(sizeof(double) * std::max<int64_t>(Tb, 1) * nsplit));
+  for (int64_t t0 = 0; t0 < T; t0 += batch) {
+    const int64_t n = std::min<int64_t>(batch, T - t0);
+    dim3 grid((unsigned)nblk(n, (int)tblk), (unsigned)nsplit);
+    if (zero_check)
+      k_far<true><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(n, txy + t0, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                                            c->d_sq.as<double>(), chunk, part.as<double>(),
+                                                            0x3ff00000u);
+    else
+      k_far<false><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(n, txy + t0, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                                             c->d_sq.as<double>(), chunk, part.as<double>(),
+                                                             0x3ff00000u);
+    k_far_reduce<<<nblk(n, 256), 256, 0, c->fs>>>(n, nsplit, part.as<double>(), ufar + t0);
+    c->far_launches += 2;
+  }
   CUDA_TRY(c, cudaGetLastError());
-  c->far_launches += 2;
   return 0;
 }
 
@@ -3459,6 +3468,11 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
       far_rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false);
       if (!far_rc && cudaEventRecord(c->ev[2], c->s2) != cudaSuccess) far_rc = set_err(c, 3, "cuda: far event");
     });
+  } else if (c->far_method == 2) {
+    // corrections only: the caller supplies the far field (subtract-and-add,
+    // SPEC.md:612-615); u = sum over N(t) and S(t) of (I_T - point sum)
+    CUDA_TRY(c, cudaMemsetAsync(c->d_ufar.p, 0, sizeof(double) * (T + 1), c->stream));
+    CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
   } else {
     if (int rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false)) return rc;
     CUDA_TRY(c, cudaEventRecord(ev[2], c->stream));
@@ -3717,7 +3731,8 @@ int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
 
 int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
   if (!c) return 1;
-  if (method != 0 && method != 1) return set_err(c, 1, "set_far_method: method must be 0 (direct) or 1 (fmm)");
+  if (method < 0 || method > 2)
+    return set_err(c, 1, "set_far_method: method must be 0 (direct), 1 (fmm) or 2 (none: corrections only)");
   if (order != 0 && (order < 4 || order > kFmmMaxP))
     return set_err(c, 1, "set_far_method: FMM order must be in [4, 62] (0 = default 31)");
   if (leaf_size < 0) return set_err(c, 1, "set_far_method: leaf size must be >= 0 (0 = default 40)");

@@ -66,20 +66,33 @@ def test_gloo_two_rank_gather_is_bit_identical(tmp_path):
 
 
 def test_bench_shards_partition_the_job():
-    """bench.py's weak-scaling shards (Morton order, contiguous equal counts)
-    cover the job's targets exactly once, and at N=1 the job is config 2."""
+    """bench.py's strong-scaling job: config 4's targets in Morton order, every
+    256th; N contiguous shards cover it exactly once at every N, and bench's
+    Morton order is the product's (dist.morton_order)."""
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench
     import paper_2205_04401_b200 as vp
+    from paper_2205_04401_b200.dist import morton_order, shard_bounds
     pr = vp.load_config(2, with_rules=False)
-    t1, n1 = bench.rank_targets(pr, 0, 1)
-    assert n1 == pr.n_tgt and np.array_equal(t1, pr.txy)
-    for world in (2, 4):
-        U = bench.job_targets(pr, world)
-        shards = [bench.rank_targets(pr, r, world) for r in range(world)]
-        assert all(n == len(U) == world * pr.n_tgt for _, n in shards)
-        assert all(len(s) == pr.n_tgt for s, _ in shards)
-        got = np.concatenate([s for s, _ in shards])
-        key = lambda a: a[np.lexsort((a[:, 1], a[:, 0]))]
-        assert np.array_equal(key(got), key(U))
+    assert np.array_equal(bench.morton_order(pr.txy), morton_order(pr.txy))
+    assert bench.auto_stride(29360128, 51380224) == 256
+    assert bench.auto_stride(184320, 331776) == 1
+    sub = bench.headline_targets(pr.txy, 8)
+    assert np.array_equal(sub, pr.txy[morton_order(pr.txy)[::8]])
+    for world in (1, 2, 4, 8):
+        parts = [bench.shard_bounds(len(sub), r, world) for r in range(world)]
+        assert parts == [shard_bounds(len(sub), r, world) for r in range(world)]
+        assert parts[0][0] == 0 and parts[-1][1] == len(sub)
+        assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+        assert max(h - l for l, h in parts) - min(h - l for l, h in parts) <= 1
+
+
+def test_bench_config_identical_across_arms():
+    """Both arms print the same config dict for the same arguments."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    a = bench.workload_config(4, 1048576, 6, 12, 1e-12, 0, 29360128, 51380224, 256, 114688, 1)
+    b = bench.workload_config(4, 1048576, 6, 12, 1e-12, 0, 29360128, 51380224, 256, 114688, 1)
+    assert a == b and a["workload"] == "config4" and a["targets"] == 114688
