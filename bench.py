@@ -415,7 +415,7 @@ def main():
         far_flop = FAR_FLOP_PER_PAIR * T * S
         peak, peak_src = fp64_peak()
         achieved = far_flop / (far_ms * 1e-3) / 1e12
-        kprof = load_json(os.path.join(HERE, "profiles", "r02_far_kernel.json")) or {}
+        kprof = load_json(os.path.join(HERE, "profiles", f"r02_far_kernel_{cfg['workload']}.json")) or {}
         kmatch = kprof.get("workload") == cfg["workload"] and kprof.get("targets") == T
         s0 = stats[-1]
 

@@ -105,6 +105,7 @@ def lib():
             "vpo_project_density": (i32, [i64, _d_p, i64, _i32_p, i32, i32, _d_p, i32, _d_p]),
             "vpo_config_info_get": (i32, [i32, i32, ctypes.c_uint64, ctypes.POINTER(VpoConfigInfo)]),
             "vpo_config_fill": (i32, [i32, i32, ctypes.c_uint64, _d_p, _i32_p, _d_p, _d_p]),
+            "vpo_adaptive_log_integral": (i32, [_d_p, i32, i32, _d_p, i64, _d_p, dbl, i32, _d_p]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)
@@ -418,3 +419,17 @@ class OracleProblem:
     @property
     def n_tgt(self):
         return self.txy.shape[0]
+
+
+def adaptive_log_integral(tri, fkind, pts, coeffs=None, p=0, tol=1e-17, nthreads=0):
+    """int_T log|x-y| f(y) dA at exterior points (adaptive subdivision, long
+    double; the soundness sweep's oracle)."""
+    tri = np.ascontiguousarray(tri, dtype=np.float64).reshape(6)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 2)
+    c = None if coeffs is None else np.ascontiguousarray(coeffs, dtype=np.float64)
+    out = np.zeros(pts.shape[0])
+    rc = lib().vpo_adaptive_log_integral(_d(tri), fkind, p, _d(c) if c is not None else None, pts.shape[0],
+                                         _d(pts), tol, nthreads, _d(out))
+    if rc:
+        raise OracleError(rc, "adaptive_log_integral: bad arguments")
+    return out

@@ -135,6 +135,13 @@ int vpo_config_fill(int config, int q_override, uint64_t seed, double* vxy, int3
                     double* coeffs);
 const char* vpo_inputs_last_error(void);
 
+/* ---- acceptance checks (vp_oracle_accept.cpp) ------------------------- */
+/* Adaptive I_T(x) = int_T log|x-y| f(y) dA at points outside the triangle
+ * tri = (ax, ay, bx, by, cx, cy); fkind 0: 1, 1: sin(x+2y), 2: exp(-x^2-y^2),
+ * 3: Koornwinder expansion of order p in T's reference coordinates. */
+int vpo_adaptive_log_integral(const double* tri, int fkind, int p, const double* coeffs, int64_t n,
+                              const double* pts, double tol, int nthreads, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,7 +4,8 @@ counters (run on the GPU box):
   python tools/fp64_flops.py OUT.json [bench args...]
 
 runs `ncu --metrics <duration, dfma/dadd/dmul thread counts>` over
-`bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-fmm` and writes, per
+`bench.py --mode pairs --steps 1 --warmup 1` (the full-size pair stage:
+far method none) and writes, per
 kernel, the FP64 flops of one launch (2 per DFMA, 1 per DADD/DMUL, the
 tensor-pipe FP64 ops of DMMA; medians
 over the run's launches -- every step does identical work) and its ncu
@@ -31,10 +32,12 @@ NEAR_STAGE = ("k_near_leaves", "k_leaves_copy", "k_near_cache", "k_near_cache_mm
 
 def main():
     out = sys.argv[1]
-    cmd = [sys.executable, "bench.py", "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-fmm"] + sys.argv[2:]
+    cmd = [sys.executable, "bench.py", "--mode", "pairs", "--steps", "1", "--warmup", "1"] + sys.argv[2:]
     log = "/tmp/fp64_flops.csv"
-    subprocess.run(["ncu", "--metrics", ",".join(MET), "--clock-control", "none", "--csv",
-                    "--log-file", log] + cmd, check=True, stdout=subprocess.DEVNULL)
+    run = subprocess.run(["ncu", "--metrics", ",".join(MET), "--clock-control", "none", "--csv",
+                          "--log-file", log] + cmd, check=True, stdout=subprocess.PIPE, text=True)
+    line = [l for l in run.stdout.splitlines() if l.startswith("{")][-1]
+    bj = json.loads(line)["pair_stage"]
     rows = list(csv.reader(io.StringIO(open(log).read())))
     h = None
     per = {}
@@ -57,8 +60,10 @@ def main():
         ns = [v.get("ns", 0) for v in launches.values()]
         res[name] = {"launches": len(fl), "fp64_flops": statistics.median(fl), "ncu_ms": statistics.median(ns) * 1e-6}
     near = {k: v for k, v in res.items() if k.split("<")[0] in NEAR_STAGE}
+    cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "4"
     doc = {"how": "ncu --metrics " + ",".join(MET) + " over " + " ".join(cmd[1:]),
-           "config_args": sys.argv[2:], "kernels": res,
+           "config_args": sys.argv[2:], "workload": f"config{cfg}", "targets": bj["targets_per_gpu"],
+           "kernels": res,
            "near_stage_fp64_flops": sum(v["fp64_flops"] for v in near.values()),
            "near_stage_kernels": sorted(near)}
     os.makedirs(os.path.dirname(out) or ".", exist_ok=True)

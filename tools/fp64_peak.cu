@@ -1,6 +1,7 @@
 // FP64 roofline denominator probe for B200 (sm_100a).
 // Measures DFMA throughput (independent chains) and DMMA m8n8k4 throughput,
-// with CUDA events, after warm-up. Prints one JSON line.
+// with CUDA events, after >= 1 s of warm-up at load (clocks ramp from idle),
+// each timed launch tens of ms long.  Prints one JSON line.
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -55,22 +56,22 @@ int main() {
   const int threads = 256, blocks = sms * 8;
   float ms = 0;
   // DFMA
-  const int it = 20000;
-  for (int w = 0; w < 3; ++w) dfma_chain<8><<<blocks, threads>>>(d, it, 0.999999, 1e-7);
+  const int it = 2000000;
+  for (int w = 0; w < 40; ++w) dfma_chain<8><<<blocks, threads>>>(d, it, 0.999999, 1e-7);
   CK(cudaDeviceSynchronize());
   double best_dfma = 0;
-  for (int r = 0; r < 5; ++r) {
+  for (int r = 0; r < 20; ++r) {
     cudaEventRecord(e0); dfma_chain<8><<<blocks, threads>>>(d, it, 0.999999, 1e-7); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double fl = 2.0 * 8 * it * (double)blocks * threads / (ms * 1e-3);
     if (fl > best_dfma) best_dfma = fl;
   }
   // DMMA: 8x8x4 per warp per mma = 2*8*8*4 = 512 flop
-  const int it2 = 20000;
-  for (int w = 0; w < 3; ++w) dmma_loop<<<blocks, threads>>>(d, it2);
+  const int it2 = 500000;
+  for (int w = 0; w < 10; ++w) dmma_loop<<<blocks, threads>>>(d, it2);
   CK(cudaDeviceSynchronize());
   double best_dmma = 0;
-  for (int r = 0; r < 5; ++r) {
+  for (int r = 0; r < 20; ++r) {
     cudaEventRecord(e0); dmma_loop<<<blocks, threads>>>(d, it2); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double fl = 512.0 * 4 * it2 * (double)blocks * (threads / 32) / (ms * 1e-3);
