@@ -15,7 +15,7 @@ OBJS := $(CSRC)/vp_b200.o $(CSRC)/vp_setup.o $(CSRC)/vp_curves.o
 
 all: $(LIB) oracle
 
-$(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/vp_curve.cuh $(CSRC)/vp_fmm.cuh \
+$(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/vp_curve.cuh $(CSRC)/vp_fmm.cuh $(CSRC)/vp_multi.cuh \
 		$(CSRC)/koorn.cuh include/vp.h include/vp_setup.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; exit 1)
 
@@ -26,7 +26,7 @@ $(CSRC)/vp_curves.o: $(CSRC)/vp_curves.cpp include/vp_setup.h
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(OBJS) -lpthread
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(OBJS) -lpthread -ldl
 
 oracle:
 	$(MAKE) -C oracle

@@ -342,7 +342,6 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2205_04401_b200 as vp
-    from paper_2205_04401_b200.dist import gather_potentials
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -359,24 +358,36 @@ def main():
     out = {}
     u_direct = None
 
-    def sharded(txy):  # this rank's Morton-contiguous shard of a Morton-ordered job
-        lo, hi = shard_bounds(len(txy), rank, world)
-        return np.ascontiguousarray(txy[lo:hi])
+    if world > 1:  # the library's own NCCL communicator carries the gather of u
+        uid = [vp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ev.comm_init(world, rank, uid[0])
 
-    def device_step(d_txy, d_u, n, n_job):
+    def sharded(txy):
+        """This rank's shard of a job: vp_shard_plan's Morton order and
+        cost-balanced bounds (for the far method currently set); at N = 1 the
+        job itself.  Returns (targets, bounds, order)."""
+        if world == 1:
+            return np.ascontiguousarray(txy), np.array([0, len(txy)]), None
+        order, bounds, _ = ev.shard_plan(txy, world)
+        return np.ascontiguousarray(txy[order[bounds[rank]:bounds[rank + 1]]]), bounds, order
+
+    def device_step(d_txy, d_u, n, bounds):
+        d_all = torch.empty(int(bounds[-1]) if world > 1 else 1, dtype=torch.float64, device=dev)
+
         def step():
             st = ev.evaluate_device(n, d_txy.data_ptr(), d_u.data_ptr(), stream.cuda_stream)
-            if world > 1:  # the only collective: gather of u (NCCL all-gather of padded shards)
-                gather_potentials(d_u, n_job, rank, world)
+            if world > 1:  # the only collective: all-gather of u (vp_gather, NCCL)
+                ev.gather(bounds, d_u.data_ptr(), d_all.data_ptr(), stream.cuda_stream)
             return st
         return step
 
     if args.mode == "all":
         sub = headline_targets(pr.txy, stride)
         cfg["targets"] = int(len(sub))
-        mine = sharded(sub)
-        T = len(mine)
         ev.set_far_method("direct")
+        mine, sub_bounds, _ = sharded(sub)
+        T = len(mine)
         # ---- parity gate + cpu_baseline: rank 0's u against the oracle (own generators)
         cpu = check = None
         if rank == 0 and not args.no_cpu_baseline:
@@ -399,7 +410,7 @@ def main():
             del octx
         d_txy = torch.from_numpy(mine).to(dev).contiguous()
         d_u = torch.empty(max(T, 1), dtype=torch.float64, device=dev)
-        step = device_step(d_txy, d_u, T, len(sub))
+        step = device_step(d_txy, d_u, T, sub_bounds)
         clk = ClockSampler(local)
         clk.start()
         clk.wait_first()
@@ -478,12 +489,13 @@ def main():
     # ---- pair stage at full size: corrections of every target (far method none)
     full = None
     if not args.no_pairs or not args.no_fmm or args.mode == "pairs":
-        full = sharded(headline_targets(pr.txy, 1))
-        d_full = torch.from_numpy(full).to(dev).contiguous()
-        d_uf = torch.empty(max(len(full), 1), dtype=torch.float64, device=dev)
-        fstep = device_step(d_full, d_uf, len(full), pr.n_tgt)
+        full_job = headline_targets(pr.txy, 1)
     if args.mode == "pairs" or not args.no_pairs:
         ev.set_far_method("none")
+        full, fb, _ = sharded(full_job)
+        d_full = torch.from_numpy(full).to(dev).contiguous()
+        d_uf = torch.empty(max(len(full), 1), dtype=torch.float64, device=dev)
+        fstep = device_step(d_full, d_uf, len(full), fb)
         n_w = 1 if args.mode == "pairs" else 2
         for _ in range(n_w):
             fstep()
@@ -526,6 +538,10 @@ def main():
     # ---- full evaluation of every target with the FMM far field
     if args.mode == "all" and not args.no_fmm:
         ev.set_far_method("fmm")
+        full, fb, _ = sharded(full_job)
+        d_full = torch.from_numpy(full).to(dev).contiguous()
+        d_uf = torch.empty(max(len(full), 1), dtype=torch.float64, device=dev)
+        fstep = device_step(d_full, d_uf, len(full), fb)
         for _ in range(2):
             fstep()
         torch.cuda.synchronize()

@@ -104,7 +104,13 @@ int vp_set_curves(vp_ctx* ctx, const int32_t* curve_id, int deg, int64_t n_curve
 
 /* Rules + tolerance; builds the per-element near-field models
  * (build_model) on the host so list predicates are
- * bit-reproducible, and the element bins used by the list build. */
+ * bit-reproducible, and the element bins used by the list build.
+ * near_eval accepts a sub-simplex once rho_d = rho0(N_n) 4^{-d/N_n} <= 1, so
+ * an element's leaves are at most d* deep; leaf path codes hold 29 levels
+ * (the reference allows 40), so an element with d* > 29
+ * (rho0 of the N_n model above 4^{29/12} = 28.5: eps far below the element's
+ * weight) is refused here with status 2.  Every BASELINE configuration has
+ * d* <= 19. */
 int vp_set_rules(vp_ctx* ctx, const vp_rules* rules);
 
 /* Density as order-p Koornwinder coefficients per triangle, [n_tri * M_p],
@@ -180,6 +186,40 @@ int vp_set_near_model(vp_ctx* ctx, int model, double ball_factor);
  * and shared by all targets, within max_bytes of HBM (0 -> 12 GiB; the depth
  * is lowered until it fits).  Values match the recurrence to rounding. */
 int vp_set_near_cache(vp_ctx* ctx, int max_depth, int64_t max_bytes);
+
+/* ---- multi-GPU ----
+ * Targets are sharded over ranks, one context (usually one process) per GPU,
+ * mesh and density replicated on every rank; the only collective is the
+ * gather of u (north_star).  NCCL is loaded at run time (libnccl.so.2). */
+
+/* Cost-balanced contiguous split of caller-supplied per-target costs (host
+ * only, no device): bounds[r] = the smallest i with sum(cost[0..i)) * world
+ * >= r * total; bounds[0] = 0, bounds[world] = n. */
+int vp_shard_bounds(int64_t n, const int64_t* cost, int world, int64_t* bounds);
+
+/* Shard plan of a target set: order_out[n_tgt] = the Morton (Z-order)
+ * permutation of the targets (16 bits per axis over their bounding box,
+ * stable), bounds_out[world+1] = a split of the Morton-ordered targets into
+ * contiguous shards of equal estimated cost (FP64 flops: the far field per
+ * the far method, |N(t)| near pairs and the self pair, from the near-field
+ * list build); shard_cost_out[world] (optional) the cost per shard.  Rank r
+ * evaluates targets order_out[bounds[r] .. bounds[r+1]). */
+int vp_shard_plan(vp_ctx* ctx, int64_t n_tgt, const double* txy, int world, int32_t* order_out,
+                  int64_t* bounds_out, int64_t* shard_cost_out);
+
+#define VP_NCCL_ID_BYTES 128
+/* NCCL unique id for vp_comm_init (rank 0 creates it; the caller ships the
+ * VP_NCCL_ID_BYTES bytes to the other ranks by its own means). */
+int vp_nccl_unique_id(unsigned char* id_out);
+/* The context's NCCL communicator: rank `rank` of `world`, on ctx's device. */
+int vp_comm_init(vp_ctx* ctx, int world, int rank, const unsigned char* id);
+/* All-gather of u: rank r's d_u_local holds targets bounds[r] .. bounds[r+1]
+ * of the job; every rank receives the whole u in d_u_all[bounds[world]]
+ * (one NCCL broadcast per shard, in a group, straight into place).
+ * Stream-ordered on `stream` (NULL: ctx stream). */
+int vp_gather(vp_ctx* ctx, const int64_t* bounds, const double* d_u_local, double* d_u_all, void* stream);
+/* vp_stats over ranks: counters summed, device times and max_depth maxed. */
+int vp_allreduce_stats(vp_ctx* ctx, vp_stats* st);
 
 /* SM count and compute capability of the context's device. */
 int vp_device_info(vp_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);

@@ -93,6 +93,13 @@ _SIGS = [
     ("vp_set_far_method", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("vp_device_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    ("vp_shard_bounds", ctypes.c_int, [ctypes.c_int64, c_int64_p, ctypes.c_int, c_int64_p]),
+    ("vp_shard_plan", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, ctypes.c_int, c_int32_p,
+                                     c_int64_p, c_int64_p]),
+    ("vp_nccl_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("vp_comm_init", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]),
+    ("vp_gather", ctypes.c_int, [ctypes.c_void_p, c_int64_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("vp_allreduce_stats", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(VpStats)]),
     # vp_setup.h
     ("vps_koorn_size", ctypes.c_int, [ctypes.c_int]),
     ("vps_gauss_legendre", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p]),

@@ -608,6 +608,35 @@ class Evaluator:
             raise NumericalError(f"[2] field_eval: {nout.value} point(s) outside domain")
         return out, eo
 
+    # ---- multi-GPU: shard plan + the library's NCCL gather
+    def shard_plan(self, txy, world: int):
+        """(order, bounds, shard_cost): Morton permutation of the targets and a
+        cost-balanced split into `world` contiguous shards (vp_shard_plan)."""
+        t = _f64(txy, (-1, 2))
+        order = np.zeros(t.shape[0], dtype=np.int32)
+        bounds = np.zeros(world + 1, dtype=np.int64)
+        cost = np.zeros(world, dtype=np.int64)
+        _check(self._L.vp_shard_plan(self._h, t.shape[0], _d(t), world, _i32(order), _i64(bounds), _i64(cost)),
+               self._err())
+        return order, bounds, cost
+
+    def comm_init(self, world: int, rank: int, uid: bytes):
+        """Join the library's NCCL communicator (uid from nccl_unique_id() on rank 0)."""
+        if len(uid) != NCCL_ID_BYTES:
+            raise UsageError(f"[1] comm_init: the unique id has {NCCL_ID_BYTES} bytes")
+        _check(self._L.vp_comm_init(self._h, world, rank, uid), self._err())
+
+    def gather(self, bounds, d_u_local: int, d_u_all: int, stream: int = 0):
+        """All-gather of u over the communicator (device pointers, stream-ordered)."""
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _check(self._L.vp_gather(self._h, _i64(b), ctypes.c_void_p(d_u_local), ctypes.c_void_p(d_u_all),
+                                 ctypes.c_void_p(stream or None)), self._err())
+
+    def allreduce_stats(self, st: dict) -> dict:
+        s = VpStats(**{k: st[k] for k, _ in VpStats._fields_})
+        _check(self._L.vp_allreduce_stats(self._h, ctypes.byref(s)), self._err())
+        return s.as_dict()
+
     def near_pairs(self, txy, elem):
         """near_eval(T, t), the point sum it replaces, and leaf counts."""
         return self._pairs(self._L.vp_near_pairs, txy, elem)
@@ -615,6 +644,28 @@ class Evaluator:
     def self_pairs(self, txy, elem):
         """self_eval(T, t), the point sum it replaces, and panel counts."""
         return self._pairs(self._L.vp_self_pairs, txy, elem)
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0), to be shipped to the other ranks."""
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    rc = _lib.lib().vp_nccl_unique_id(buf)
+    if rc != 0:
+        raise DeviceError(f"[{rc}] vp_nccl_unique_id: NCCL unavailable")
+    return buf.raw
+
+
+def shard_bounds(cost, world: int) -> np.ndarray:
+    """Cost-balanced contiguous split of per-target costs (vp_shard_bounds, host only)."""
+    c = np.ascontiguousarray(cost, dtype=np.int64)
+    b = np.zeros(world + 1, dtype=np.int64)
+    rc = _lib.lib().vp_shard_bounds(c.size, _i64(c), world, _i64(b))
+    if rc != 0:
+        raise UsageError("[1] shard_bounds: need world >= 1 and non-negative costs")
+    return b
 
 
 def evaluate_field(pr: Problem, targets=None, device: int = 0):

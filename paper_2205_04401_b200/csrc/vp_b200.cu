@@ -609,7 +609,36 @@ constexpr int kLeafScratchMax = VP_LEAF_SCRATCH_MAX;
 #ifndef VP_LEAVES_MINB
 #define VP_LEAVES_MINB 5
 #endif
-template <bool FILL>
+// Pending rejected children of the precise-model walk, one 4-bit mask per
+// level 1..kMaxPathDepth in two registers (levels 1-16 in lo, 17-32 in hi):
+// the depth-first order of a path-code stack without its local memory.
+struct LevelMasks {
+  unsigned long long lo = 0, hi = 0;
+  __device__ __forceinline__ void set(int l, unsigned m) {
+    if (l <= 16) lo |= (unsigned long long)m << (4 * (l - 1));
+    else hi |= (unsigned long long)m << (4 * (l - 17));
+  }
+  __device__ __forceinline__ bool empty() const { return (lo | hi) == 0ull; }
+  // deepest level with a pending child and its lowest pending child, cleared
+  __device__ __forceinline__ void pop(int& l, int& j) {
+    if (hi) {
+      const int b = 63 - __clzll((long long)hi);
+      l = 17 + b / 4;
+      const unsigned nib = (unsigned)(hi >> (4 * (l - 17))) & 15u;
+      j = __ffs(nib) - 1;
+      hi &= ~(1ull << (4 * (l - 17) + j));
+    } else {
+      const int b = 63 - __clzll((long long)lo);
+      l = 1 + b / 4;
+      const unsigned nib = (unsigned)(lo >> (4 * (l - 1))) & 15u;
+      j = __ffs(nib) - 1;
+      lo &= ~(1ull << (4 * (l - 1) + j));
+    }
+  }
+};
+static_assert(kMaxPathDepth <= 32, "LevelMasks holds 32 levels");
+
+template <bool FILL, bool BALL>
 __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
     k_near_leaves(int64_t n_pairs, const int32_t* __restrict__ pair_tgt,
                   const int32_t* __restrict__ pair_elem, const double2* __restrict__ txy,
@@ -621,7 +650,7 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
   __shared__ double skd[kMaxNearDepth + 2];
   for (int i = threadIdx.x; i < kMaxNearDepth + 2; i += blockDim.x) skd[i] = R->kd[i];
   __syncthreads();
-  const double ball_factor = R->near_model == 1 ? R->ball_factor : 0.0;
+  const double ball_factor = BALL ? R->ball_factor : 0.0;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -636,7 +665,13 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
   double l0[3];
   int gd = -1;
   double gv = 0.0;
-  unsigned long long stack[kStackCap];
+  // precise model: the node to expand next (path, depth; cd < 0: the root is
+  // not tested yet) and the pending rejected children per level
+  unsigned long long cpath = 0;
+  int cd = -1;
+  LevelMasks pend;
+  // ball model: a stack of path codes (node-by-node walk, depth <= 20)
+  unsigned long long stack[BALL ? 3 * kBallMaxDepth + 4 : 1];
   int sp = 0;
   int64_t n = 0, nc = 0, oc = 0, od = 0;
   while (true) {
@@ -655,8 +690,14 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
           E = el[pair_elem[p]];
           side_lengths0(E, l0);
           gd = -1;
-          sp = 0;
-          stack[sp++] = ball_factor == 0.0 ? (1ull << 57) : 0ull;  // precise model: root untested
+          if (BALL) {
+            sp = 0;
+            stack[sp++] = 0ull;
+          } else {
+            cpath = 0;
+            cd = -1;
+            pend = LevelMasks();
+          }
           n = nc = 0;
           if (FILL) {
             oc = lo.offc[p];
@@ -671,24 +712,22 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
       continue;
     }
     if (!act) continue;
-    bool bad = false;
-    if (ball_factor == 0.0) {
+    bool bad = false, done = false;
+    if (!BALL) {
       // precise model: one step expands a rejected node, testing its four
       // children together.  The children's 12 vertex distances are 6 distinct
       // ones (a, b, c, m_ab, m_bc, m_ca; a shared vertex has the same
       // reference coordinates, hence bit-identical distance), so a child test
       // costs 1.5 square roots instead of 3.  Accepted children are emitted in
-      // child order, rejected ones pushed (child 0 on top); the leaf set and
-      // the counters are those of near_accept node by node.  The root is
-      // tested first (`code` bit 57 marks a node not tested yet).
-      const unsigned long long code = stack[--sp];
-      const int d = (int)(code >> 58);
-      // (a depth-0 code has path 0, so bit 57 can mark it; deeper paths use it)
-      const bool untested_root = d == 0 && (code & (1ull << 57));
-      const unsigned long long path = untested_root ? 0ull : code & kPathMask;
-      double ax, ay, bx, by, cx, cy;
-      decode_path_i(path, d, ax, ay, bx, by, cx, cy);
-      if (untested_root) {
+      // child order; rejected ones become pending at their level and are
+      // expanded depth-first, lowest child first.  The leaf set and every
+      // counter are those of near_accept node by node (the oracle's near_rec);
+      // the order of a pair's leaves differs from the oracle's recursion (an
+      // accepted child is emitted before the subtrees of its rejected lower
+      // siblings), which only reorders the per-pair sum.
+      if (cd < 0) {  // the root
+        double ax, ay, bx, by, cx, cy;
+        decode_path_i(0ull, 0, ax, ay, bx, by, cx, cy);
         bool le1;
         if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[0]), ax, ay, bx, by, cx, cy, le1, 0, 0.0, l0, gd, gv)) {
           if (FILL) {
@@ -700,10 +739,15 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
           ++n;
           nc += 0 <= lo.D ? 1 : 0;
           rle1 += le1 ? 1ull : 0ull;
+          done = true;
         } else {
-          stack[sp++] = 0ull;
+          cd = 0;
         }
       } else {
+        const int d = cd;
+        const unsigned long long path = cpath;
+        double ax, ay, bx, by, cx, cy;
+        decode_path_i(path, d, ax, ay, bx, by, cx, cy);
         const int dc = d + 1;
         const double rd = rn_mul(E.rho0n, skd[dc]);
         const unsigned long long base = ((unsigned long long)dc << 58) | (path << 2);
@@ -741,9 +785,13 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
             acc4[j] = !in;
           }
         }
+        unsigned rej = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          if (!acc4[j]) continue;
+          if (!acc4[j]) {
+            rej |= 1u << j;
+            continue;
+          }
           const unsigned long long cc = base | (unsigned long long)j;
           if (FILL) {
             if (dc <= lo.D) lo.leafc[oc++] = tag_cached(cc, pair_elem[p]);
@@ -756,46 +804,52 @@ __global__ void __launch_bounds__(128, VP_LEAVES_MINB)
           rle1 += le1 ? 1ull : 0ull;
           maxd = max(maxd, dc);
         }
-#pragma unroll
-        for (int j = 3; j >= 0; --j) {
-          if (acc4[j]) continue;
-          if (dc + 1 > kMaxPathDepth || sp + 1 > kStackCap) {
-            bad = true;
-            break;
+        if (rej) {
+          if (dc + 1 > kMaxPathDepth) bad = true;  // excluded on the host (vp_set_rules)
+          else pend.set(dc, rej);
+        }
+        if (!bad) {
+          if (pend.empty()) {
+            done = true;
+          } else {
+            int l, j;
+            pend.pop(l, j);
+            cpath = ((path >> (2 * (dc - l))) << 2) | (unsigned long long)j;
+            cd = l;
           }
-          stack[sp++] = base | (unsigned long long)j;
         }
       }
     } else {
-    // ball model: one node of this lane's pair per step
-    const unsigned long long code = stack[--sp];
-    const int d = (int)(code >> 58);
-    const unsigned long long path = code & kPathMask;
-    double ax, ay, bx, by, cx, cy;
-    decode_path_i(path, d, ax, ay, bx, by, cx, cy);
-    bool le1;
-    if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd, gv)) {
-      if (FILL) {
-        if (d <= lo.D) lo.leafc[oc++] = tag_cached(code, pair_elem[p]);
-        else lo.leafd[od++] = code;
-      } else if (n < cap) {
-        scratch[p * cap + n] = code;
+      // ball model: one node of this lane's pair per step
+      const unsigned long long code = stack[--sp];
+      const int d = (int)(code >> 58);
+      const unsigned long long path = code & kPathMask;
+      double ax, ay, bx, by, cx, cy;
+      decode_path_i(path, d, ax, ay, bx, by, cx, cy);
+      bool le1;
+      if (near_accept(E, tx, ty, rn_mul(E.rho0n, skd[d]), ax, ay, bx, by, cx, cy, le1, d, ball_factor, l0, gd, gv)) {
+        if (FILL) {
+          if (d <= lo.D) lo.leafc[oc++] = tag_cached(code, pair_elem[p]);
+          else lo.leafd[od++] = code;
+        } else if (n < cap) {
+          scratch[p * cap + n] = code;
+        }
+        ++n;
+        nc += d <= lo.D ? 1 : 0;
+        rle1 += le1 ? 1ull : 0ull;
+        maxd = max(maxd, d);
+      } else if (d + 1 > kBallMaxDepth) {
+        bad = true;
+      } else {
+        const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
+        stack[sp++] = base | 3ull;
+        stack[sp++] = base | 2ull;
+        stack[sp++] = base | 1ull;
+        stack[sp++] = base;
       }
-      ++n;
-      nc += d <= lo.D ? 1 : 0;
-      rle1 += le1 ? 1ull : 0ull;
-      maxd = max(maxd, d);
-    } else if (d + 1 > kMaxPathDepth || sp + 4 > kStackCap) {
-      bad = true;
-    } else {
-      const unsigned long long base = ((unsigned long long)(d + 1) << 58) | (path << 2);
-      stack[sp++] = base | 3ull;
-      stack[sp++] = base | 2ull;
-      stack[sp++] = base | 1ull;
-      stack[sp++] = base;
+      done = sp == 0;
     }
-    }
-    if (bad || sp == 0) {  // the pair is done
+    if (bad || done) {  // the pair is done
       if (bad) atomicExch(err, 2);
       if (!FILL) {
         if (bad) n = nc = 0;
@@ -2428,6 +2482,11 @@ struct vp_ctx {
   // far-field method: 0 direct (K2), 1 FMM
   int far_method = 0, fmm_p = 31, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
   int64_t fmm_outside = 0;
+  int max_near_depth = 0;  // deepest near_eval leaf any element can produce (build_elements)
+  bool elems_ok = false;   // the last build_elements succeeded
+  // multi-GPU (vp_multi.cuh): the library's NCCL communicator, if any
+  void* comm = nullptr;
+  int comm_world = 0, comm_rank = -1;
   DevBuf d_selftab;
   int selftab_p = -1;
   // near-leaf density cache (depth <= cache_depth sub-simplices), see k_near_cache
@@ -2440,8 +2499,7 @@ struct vp_ctx {
   DevBuf d_tl;  // per-target cached-leaf ranges (k_tgt_leafrange)
   DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
   DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
-  int64_t leaf_scratch_budget = 4ll << 30;  // bytes for the count pass's leaf scratch
-  int64_t free_mem_at_first_near = -1;
+  int64_t leaf_scratch_budget = 4ll << 30;  // max bytes of the count pass's leaf scratch (VP_LEAF_SCRATCH_BYTES)
   int tabs_p = -1;  // p of the density-independent tables (K1's V, near-cache Vt, SelfTab); -1: stale
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tk, f_tk2, f_tv, f_tord;  // FMM: target leaf keys and the leaf order of the targets
@@ -2462,6 +2520,8 @@ struct vp_ctx {
 };
 
 namespace {
+
+void vp_comm_release(vp_ctx* c);  // vp_multi.cuh
 
 int set_err(vp_ctx* c, int code, const std::string& m) {
   if (c) {
@@ -2503,6 +2563,8 @@ int build_elements(vp_ctx* c) {
   const double cq = cn_lookup(r.q), cnn = cn_lookup(r.n_n);
   std::vector<ElemRec> h(E);
   c->h_allnear.clear();
+  c->max_near_depth = 0;
+  c->elems_ok = false;
   double gx0 = 1e300, gy0 = 1e300, gx1 = -1e300, gy1 = -1e300;
   std::vector<double> ext;
   ext.reserve(E);
@@ -2536,6 +2598,20 @@ int build_elements(vp_ctx* c) {
     const double wnn = wn * R.det;
     const double denn = r.eps * cnn;
     R.rho0n = std::pow(wnn / denn, 1.0 / (double)r.n_n);
+    if (c->near_model == 0) {
+      // near_eval accepts every sub-simplex with rho_d = rho0n 4^{-d/N_n} <= 1
+      // (SURVEY.md §9.4), so no leaf is deeper than the first such d.  The
+      // path codes hold kMaxPathDepth levels (the oracle errors only past
+      // kMaxNearDepth = 40): refuse elements that could need more.
+      int dstar = 0;
+      while (dstar <= kMaxNearDepth && R.rho0n * c->h_rd.kd[dstar] > 1.0) ++dstar;
+      if (dstar > kMaxPathDepth)
+        return set_err(c, 2, "set_rules: element " + std::to_string(e) + " could need near_eval depth " +
+                                 std::to_string(dstar) + " > " + std::to_string(kMaxPathDepth) +
+                                 " (path-code limit; rho0 of the N_n model too large: eps too small for the "
+                                 "element size)");
+      c->max_near_depth = std::max(c->max_near_depth, dstar);
+    }
     if (c->near_model == 1) {  // ball model, same operations as the oracle's ball_of
       const double bxr = px[1] - px[0], byr = py[1] - py[0], cxr = px[2] - px[0], cyr = py[2] - py[0];
       const double t1 = bxr * cyr, t2 = byr * cxr;
@@ -2656,6 +2732,7 @@ int build_elements(vp_ctx* c) {
                                                              c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>());
   CUDA_TRY(c, cudaGetLastError());
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->elems_ok = true;
   return 0;
 }
 
@@ -2816,23 +2893,31 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_loffc.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_loffd.ensure(sizeof(int64_t) * (n + 1)));
   CUDA_TRY(c, c->d_ldeep.ensure(sizeof(int32_t) * (n + 1)));
-  // scratch for the first `cap` leaves of every pair, within a memory budget:
-  // the larger of leaf_scratch_budget and 10 % of the free device memory
-  // (free memory is sampled once per context: no driver query per evaluation)
-  if (c->free_mem_at_first_near < 0) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
-    c->free_mem_at_first_near = (int64_t)free_b;
+  // scratch for the first `cap` leaves of every pair (pairs with more are
+  // walked again), within a budget: a quarter of the free device memory, at
+  // most leaf_scratch_budget (VP_LEAF_SCRATCH_BYTES, default 4 GiB) beyond
+  // what the context already holds; halved until the allocation succeeds
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    free_b = 0;
   }
-  const int64_t budget = std::max<int64_t>(c->leaf_scratch_budget, c->free_mem_at_first_near / 10);
-  const int cap = (int)std::min<int64_t>(kLeafScratchMax, (budget / 8) / std::max<int64_t>(n, 1));
-  CUDA_TRY(c, c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)));
+  int64_t budget = std::min<int64_t>(c->leaf_scratch_budget, (int64_t)(free_b / 4) + (int64_t)c->d_lscratch.cap);
+  int cap = 0;
+  for (;;) {
+    cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLeafScratchMax, (budget / 8) / std::max<int64_t>(n, 1)));
+    if (c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)) == cudaSuccess) break;
+    cudaGetLastError();
+    if (cap == 1) return set_err(c, 3, "near_eval: out of device memory for the leaf scratch");
+    budget /= 2;
+  }
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
   CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_nover.p, 0, 2 * sizeof(unsigned), c->stream));
   LeafOut lo{c->d_lcntc.as<int64_t>(), c->d_lcntd.as<int64_t>(), c->d_loffc.as<int64_t>(), c->d_loffd.as<int64_t>(),
              nullptr, nullptr, c->d_ldeep.as<int32_t>(), c->d_nover.as<unsigned>() + 1, c->cache_depth, pelem};
-  k_near_leaves<false><<<nblk(n, 4 * kLeafChunk), 128, 0, c->stream>>>(
+  (c->near_model == 1 ? k_near_leaves<false, true> : k_near_leaves<false, false>)<<<nblk(n, 4 * kLeafChunk), 128, 0,
+                                                                                     c->stream>>>(
       n, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), c->d_lcnt.as<int64_t>(), lo,
       c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), nullptr,
       c->d_lscratch.as<unsigned long long>(), cap, c->d_lover.as<int32_t>(), c->d_nover.as<unsigned>(), kLeafChunk);
@@ -2862,7 +2947,8 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   k_leaves_copy<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->d_lcnt.as<int64_t>(), cap,
                                                      c->d_lscratch.as<unsigned long long>(), lo);
   if (nover > 0)
-    k_near_leaves<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
+    (c->near_model == 1 ? k_near_leaves<true, true> : k_near_leaves<true, false>)<<<nblk(nover, 128), 128, 0,
+                                                                                   c->stream>>>(
         nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, lo,
         c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0,
         nullptr, nullptr, 32);
@@ -3183,6 +3269,8 @@ int ensure_ready(vp_ctx* c, bool need_density) {
   if (!c->have_mesh) return set_err(c, 1, "usage: vp_set_mesh must precede evaluation");
   if (!c->have_rules) return set_err(c, 1, "usage: vp_set_rules must precede evaluation");
   if (need_density && !c->have_density) return set_err(c, 1, "usage: vp_set_density must precede evaluation");
+  if (!c->elems_ok)
+    return set_err(c, 1, "usage: the mesh and rules were rejected by vp_set_mesh/vp_set_rules (see that error)");
   return 0;
 }
 
@@ -3451,6 +3539,19 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   // timing stays clean.
   const bool overlap = c->far_method == 1;
   int far_rc = 0;
+  // on an error return after s2/s3 were forked, wait for their work (it reads
+  // the caller's targets and updates d_stats) before the next call reuses the
+  // buffers; declared first, so it runs after FarJoin joined the far thread
+  struct ForkGuard {
+    vp_ctx* c;
+    bool ok = false;
+    ~ForkGuard() {
+      if (!ok) {
+        cudaStreamSynchronize(c->s3);
+        cudaStreamSynchronize(c->s2);
+      }
+    }
+  } fork_guard{c};
   std::thread far_thread;
   struct FarJoin {  // joins on every return path and restores the far stream
     vp_ctx* c;
@@ -3569,6 +3670,7 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     cudaEventElapsedTime(&tot, ev[0], ev[5]);
     st->t_total_ms = tot;
   }
+  fork_guard.ok = true;
   return 0;
 }
 
@@ -3596,6 +3698,10 @@ int vp_create(int device, vp_ctx** out) {
   vp_ctx* c = new vp_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
+  if (const char* lb = std::getenv("VP_LEAF_SCRATCH_BYTES")) {
+    const long long v = std::atoll(lb);
+    if (v > 0) c->leaf_scratch_budget = v;
+  }
   // the main stream (lists, near chain) outranks s2 (FMM far) and s3 (self,
   // point sums), which fill the SMs the near chain leaves free
   int prio_lo = 0, prio_hi = 0;
@@ -3699,6 +3805,7 @@ void vp_destroy(vp_ctx* c) {
   if (c->s2) cudaStreamDestroy(c->s2);
   if (c->s3) cudaStreamDestroy(c->s3);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm) vp_comm_release(c);
   delete c;
 }
 
@@ -4262,3 +4369,5 @@ int vp_self_pairs(vp_ctx* c, int64_t n, const double* txy, const int32_t* elem, 
 }
 
 }  // extern "C"
+
+#include "vp_multi.cuh"

@@ -96,3 +96,23 @@ def test_bench_config_identical_across_arms():
     a = bench.workload_config(4, 1048576, 6, 12, 1e-12, 0, 29360128, 51380224, 256, 114688, 1)
     b = bench.workload_config(4, 1048576, 6, 12, 1e-12, 0, 29360128, 51380224, 256, 114688, 1)
     assert a == b and a["workload"] == "config4" and a["targets"] == 114688
+
+
+def test_shard_bounds_host():
+    """vp_shard_bounds (host only): contiguous cover, balanced to one item's
+    cost, equal to a numpy restatement of its definition."""
+    import paper_2205_04401_b200 as vp
+    rng = np.random.default_rng(5)
+    for n, world in [(0, 3), (1, 4), (10, 3), (1000, 8), (12345, 7)]:
+        cost = rng.integers(0, 1000, size=n).astype(np.int64)
+        b = vp.shard_bounds(cost, world)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        P = np.concatenate([[0], np.cumsum(cost)])
+        ref = [0] + [int(np.searchsorted(P * world >= r * P[-1], True)) if False else
+                     int(np.argmax(P * world >= r * P[-1])) for r in range(1, world)] + [n]
+        assert list(b) == ref
+        if n:
+            per = [P[b[r + 1]] - P[b[r]] for r in range(world)]
+            assert max(per) <= P[-1] / world + cost.max()
+    with pytest.raises(vp.UsageError):
+        vp.shard_bounds([1, -1], 2)
