@@ -89,6 +89,8 @@ def parse():
     ap.add_argument("--no-pairs", action="store_true", help="skip the full-size pair-stage measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the oracle check / cpu_baseline")
     ap.add_argument("--ref-chunk", type=int, default=0, help="--impl reference: targets per step (0: auto)")
+    ap.add_argument("--near-cache-depth", type=int, default=3, help="vp_set_near_cache max depth")
+    ap.add_argument("--near-cache-gb", type=float, default=0, help="vp_set_near_cache byte budget (0: library default)")
     return ap.parse_args()
 
 
@@ -351,6 +353,8 @@ def main():
     S = pr.n_tri * len_q
     stride = args.stride or auto_stride(pr.n_tgt, S)
     ev = vp.Evaluator(local).load(pr)
+    if args.near_cache_gb or args.near_cache_depth != 3:
+        ev.set_near_cache(args.near_cache_depth, int(args.near_cache_gb * (1 << 30)))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     cfg = workload_config(args.config, pr.n_tri, pr.p, pr.q, pr.eps, args.seed, pr.n_tgt, S, stride,

@@ -183,8 +183,9 @@ int vp_set_near_model(vp_ctx* ctx, int model, double ball_factor);
 
 /* Near-leaf density cache: w_i f at the N_n-rule nodes of every sub-simplex
  * of depth <= max_depth (-1 disables; default 3) is precomputed per element
- * and shared by all targets, within max_bytes of HBM (0 -> 12 GiB; the depth
- * is lowered until it fits).  Values match the recurrence to rounding. */
+ * and shared by all targets, within max_bytes of HBM (0 -> min(48 GiB, a
+ * quarter of the free device memory); the depth is lowered until it fits).
+ * Values match the recurrence to rounding. */
 int vp_set_near_cache(vp_ctx* ctx, int max_depth, int64_t max_bytes);
 
 /* ---- multi-GPU ----

@@ -1629,33 +1629,69 @@ __global__ void k_near_combine(int64_t n, const double* __restrict__ a, const do
 // q_i log r^2.  Warp per target, lanes over the flattened (element, source)
 // items, so one reduction serves all of t's pairs.  Coincident pairs take the
 // far sum's own no-zero-check log and cancel with it.
+// The log table is replicated COPIES times (entry k, copy c at k COPIES + c;
+// lane l reads copy l mod COPIES).  One copy has half its shared wavefronts
+// bank-conflicted, but the kernel waits on its gathers (long_scoreboard):
+// config 4 measured 19.9 / 20.3 / 21.0 / 28.8 ms with 1 / 2 / 4 / 8 copies
+// (VP_PSUM_COPIES), so the default is one.
 constexpr int PT_WARPS = 8;
+template <int COPIES>
 __global__ void __launch_bounds__(PT_WARPS * 32)
     k_psum_tgt(int64_t T, const double2* __restrict__ txy, const int32_t* __restrict__ self,
                const int64_t* __restrict__ off, const int32_t* __restrict__ ids, int len_q,
                const double* __restrict__ sx, const double* __restrict__ sy, const double* __restrict__ sq,
                double* __restrict__ psum) {
-  __shared__ double2 sltab[kLogEntries];
-  for (int i = threadIdx.x; i < kLogEntries; i += blockDim.x) sltab[i] = g_logtab[i];
+  extern __shared__ __align__(16) double2 ptab[];
+  for (int i = threadIdx.x; i < kLogEntries * COPIES; i += blockDim.x) ptab[i] = g_logtab[i / COPIES];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double2* sltab = ptab + (lane & (COPIES - 1));
+  // Items (element b of S(t) u N(t), source i) flattened over the lanes, four
+  // per lane and pass with every load issued before the logs; the element id
+  // comes from lane b of a per-target register list (one coalesced load) and
+  // b = j / len_q from a multiply-high (exact for j < 32 * 600, len_q < 600).
+  const unsigned magic = (unsigned)((1ull << 32) / (unsigned)len_q + 1ull);
   for (int64_t t = (int64_t)blockIdx.x * PT_WARPS + wid; t < T; t += (int64_t)gridDim.x * PT_WARPS) {
     const double2 tp = txy[t];
     const int32_t se = self[t];
     const int64_t o0 = off[t], nn = off[t + 1] - o0;
-    const int first = se >= 0 ? 0 : 1;  // item block 0 = S(t), blocks 1.. = N(t)
-    const int64_t items = (nn + 1 - first) * (int64_t)len_q;
-    double s = 0.0;
-    int blk = first + lane / len_q, src = lane - (lane / len_q) * len_q;
-    for (int64_t j = lane; j < items; j += 32) {
-      const int32_t e = blk == 0 ? se : ids[o0 + blk - 1];
-      const int64_t k = (int64_t)e * len_q + src;
-      const double dx = tp.x - sx[k], dy = tp.y - sy[k];
-      s = fma(sq[k], fast_log_r2<1, false>(sltab, fma(dx, dx, dy * dy)), s);
-      src += 32;
-      while (src >= len_q) { src -= len_q; ++blk; }
+    const int hs = se >= 0 ? 1 : 0;
+    const int64_t nb = nn + hs;
+    double s = 0.0, s1 = 0.0;
+    if (nb <= 32 && len_q < 600) {
+      const int32_t my_e = lane < nb ? (lane < hs ? se : ids[o0 + lane - hs]) : 0;
+      const int items = (int)nb * len_q;
+      for (int j0 = 0; j0 < items; j0 += 128) {
+        double xs[4], ys[4], qs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + lane + 32 * u;
+          const int jj = j < items ? j : 0;
+          const int bb = (int)__umulhi((unsigned)jj, magic);
+          const int32_t e = __shfl_sync(0xffffffffu, my_e, bb);
+          const int64_t k = (int64_t)e * len_q + (jj - bb * len_q);
+          xs[u] = sx[k];
+          ys[u] = sy[k];
+          qs[u] = j < items ? sq[k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double dx = tp.x - xs[u], dy = tp.y - ys[u];
+          double& a = (u & 1) ? s1 : s;
+          a = fma(qs[u], fast_log_r2<COPIES, false>(sltab, fma(dx, dx, dy * dy)), a);
+        }
+      }
+    } else {  // long lists (all-near elements): element by element
+      for (int64_t b = 0; b < nb; ++b) {
+        const int32_t e = b < hs ? se : ids[o0 + b - hs];
+        for (int j = lane; j < len_q; j += 32) {
+          const int64_t k = (int64_t)e * len_q + j;
+          const double dx = tp.x - sx[k], dy = tp.y - sy[k];
+          s = fma(sq[k], fast_log_r2<COPIES, false>(sltab, fma(dx, dx, dy * dy)), s);
+        }
+      }
     }
-    s = warp_sum(s);
+    s = warp_sum(s + s1);
     if (lane == 0) psum[t] = s;
   }
 }
@@ -1703,11 +1739,17 @@ __device__ __forceinline__ void self_geom(double tx, double ty, double Ax, doubl
 }
 
 // panel boundary b_i, i = 0 .. N+M+2
+// 2^-i for 0 <= i <= 1022, exact (scaling by it is ldexp(x, -i) while the
+// result stays normal: here x >= 2^i dmin > 0)
+__device__ __forceinline__ double pow2m(int i) { return __longlong_as_double((long long)(1023 - i) << 52); }
 __device__ __forceinline__ double self_bnd(const SelfGeom& G, int i) {
   if (i == 0) return 0.0;
-  if (i <= G.N) return rn_sub(G.st, ldexp(G.st, -i));
+  if (i <= G.N) return rn_sub(G.st, i <= 1022 ? G.st * pow2m(i) : ldexp(G.st, -i));
   if (i == G.N + 1) return G.st;
-  if (i <= G.N + G.Mr + 1) return rn_add(G.st, ldexp(rn_sub(G.L, G.st), -(G.Mr + 1 - (i - G.N - 1))));
+  if (i <= G.N + G.Mr + 1) {
+    const int k = G.Mr + 1 - (i - G.N - 1);
+    return rn_add(G.st, k <= 1022 ? rn_sub(G.L, G.st) * pow2m(k) : ldexp(rn_sub(G.L, G.st), -k));
+  }
   return G.L;
 }
 
@@ -1747,7 +1789,7 @@ struct SelfTab {
 // the 3 x 2(p+1) moment polynomials one more; only the arc-length nodes
 // (dyadic panels x Gauss-Legendre) go side by side.
 struct SelfSide {
-  double Ax, Ay, ABx, ABy, L, h, st, avx, avy, BRx, BRy;
+  double Ax, Ay, ABx, ABy, L, h, st, avx, avy, BRx, BRy, invL;
   int N, Mr, npan, degenerate, pad;
 };
 template <int P>
@@ -1769,7 +1811,10 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   constexpr int SNPT = SNPT0 < VP_SELF_SNPT_MAX ? SNPT0 : VP_SELF_SNPT_MAX;
   __shared__ double scc[SELF_WARPS][M];
   __shared__ double sF[SELF_WARPS][M3], sE[SELF_WARPS][3][2 * NP];
-  __shared__ double sB[SELF_WARPS][kMaxSelfPanels + 1];
+  // non-empty panels of the side in progress: sl = a + b x_gl (panel middle and
+  // half width over L), weight h (half width) w_gl
+  __shared__ double sPa[SELF_WARPS][kMaxSelfPanels + 4], sPb[SELF_WARPS][kMaxSelfPanels + 4],
+      sPc[SELF_WARPS][kMaxSelfPanels + 4];
   __shared__ SelfSide sS[SELF_WARPS][3];
   constexpr bool kHorner = P <= kSelfHornerMaxP;
   extern __shared__ __align__(16) double sT2[];  // [2 NP][M], dynamic
@@ -1828,6 +1873,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
       SelfSide& S = sS[wid][k];
       S.Ax = G.Ax; S.Ay = G.Ay; S.ABx = G.ABx; S.ABy = G.ABy; S.L = G.L; S.h = G.h; S.st = G.st;
+      S.invL = 1.0 / G.L;
       S.avx = Arx - txi;  // A - v in reference coordinates
       S.avy = Ary - teta;
       S.BRx = (k == 0 ? 1.0 : 0.0) - Arx;
@@ -1893,57 +1939,91 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       G.N = S.N; G.Mr = S.Mr;
       const double* Eb = sE[wid][k];
       const double* Ec = Eb + NP;
-      // (3) arc-length nodes: dyadic panels x Gauss-Legendre;
-      // the panel boundaries once per side in shared memory
+      // (3) arc-length nodes: dyadic panels x Gauss-Legendre.
+      // The side's non-empty panels are compacted once (ballot) into (a, b, c)
+      // with sl = s / L = a + b x_gl and node weight c w_gl = (half width) h w_gl,
+      // so the node loop has no empty-panel test; the side's sigma polynomials
+      // (Eb pre-halved: log r0 = log(r0^2) / 2) sit in registers.
       const int npan = S.npan;
-      for (int i = lane; i <= npan; i += 32) sB[wid][i] = self_bnd(G, i);
+      const double invL = S.invL;
+      int nne = 0;
+      for (int i0 = 0; i0 < npan; i0 += 32) {
+        const int i = i0 + lane;
+        const double s0 = i <= npan ? self_bnd(G, i) : 0.0;
+        double s1 = __shfl_down_sync(0xffffffffu, s0, 1);
+        if (lane == 31) s1 = i + 1 <= npan ? self_bnd(G, i + 1) : 0.0;
+        const bool ne = i < npan && s1 > s0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ne);
+        if (ne) {
+          const int pos = nne + __popc(bal & ((1u << lane) - 1u));
+          const double half = 0.5 * (s1 - s0);
+          sPa[wid][pos] = (0.5 * (s0 + s1)) * invL;
+          sPb[wid][pos] = half * invL;
+          sPc[wid][pos] = half * G.h;
+        }
+        nne += __popc(bal);
+      }
+      npan_item += nne;
+      if (lane < 4) {  // zero-weight pad panels: the paired node loop needs no bound test
+        sPa[wid][nne + lane] = 0.0;
+        sPb[wid][nne + lane] = 0.0;
+        sPc[wid][nne + lane] = 0.0;
+      }
       __syncwarp();
-      const int nodes = npan * NL;
-      const double invL = 1.0 / G.L;
-      int pi = lane / NL, gq = lane - pi * NL;
-      for (int j = lane; j < nodes; j += 32, gq += 32) {
-        while (gq >= NL) { gq -= NL; ++pi; }
-        const double s0 = sB[wid][pi], s1 = sB[wid][pi + 1];
-        if (!(s1 > s0)) continue;
-        const double mid = 0.5 * (s0 + s1), half = 0.5 * (s1 - s0);
-        const double s = fma(half, sglx[gq], mid);
-        const double ws = half * sglw[gq];
-        const double sl = s * invL;
-        const double px = fma(sl, G.ABx, G.Ax), py = fma(sl, G.ABy, G.Ay);
-        const double ddx = px - tx, ddy = py - ty;
-        const double lr0 = 0.5 * fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
+      double eb[NP], ec[NP];
+#pragma unroll
+      for (int kk = 0; kk < NP; ++kk) {
+        eb[kk] = 0.5 * Eb[kk];
+        ec[kk] = Ec[kk];
+      }
+      const double dAx = G.Ax - tx, dAy = G.Ay - ty;
+      auto node = [&](int pp, double xg, double wg) {
+        const double sl = fma(sPb[wid][pp], xg, sPa[wid][pp]);
+        const double ddx = fma(sl, G.ABx, dAx), ddy = fma(sl, G.ABy, dAy);
+        const double lg = fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
         const double x = fma(2.0, sl, -1.0);
         double ib, ic;
         if constexpr (kHorner) {
-          ib = Eb[NP - 1];
-          ic = Ec[NP - 1];
+          ib = eb[NP - 1];
+          ic = ec[NP - 1];
 #pragma unroll
           for (int kk = NP - 2; kk >= 0; --kk) {
-            ib = fma(ib, x, Eb[kk]);
-            ic = fma(ic, x, Ec[kk]);
+            ib = fma(ib, x, eb[kk]);
+            ic = fma(ic, x, ec[kk]);
           }
         } else {
           double q0 = 1.0, q1 = x;
-          ib = Eb[0];
-          ic = Ec[0];
+          ib = eb[0];
+          ic = ec[0];
           if (NP > 1) {
-            ib = fma(Eb[1], q1, ib);
-            ic = fma(Ec[1], q1, ic);
+            ib = fma(eb[1], q1, ib);
+            ic = fma(ec[1], q1, ic);
           }
 #pragma unroll
           for (int kk = 1; kk + 1 < NP; ++kk) {
             const double q2 = fma(sla[kk] * x, q1, -slb[kk] * q0);
-            ib = fma(Eb[kk + 1], q2, ib);
-            ic = fma(Ec[kk + 1], q2, ic);
+            ib = fma(eb[kk + 1], q2, ib);
+            ic = fma(ec[kk + 1], q2, ic);
             q0 = q1;
             q1 = q2;
           }
         }
-        acc = fma(ws * G.h, fma(lr0, ib, ic), acc);
-      }
-      for (int i = 0; i < npan; i += 32) {
-        const bool nonempty = i + lane < npan && sB[wid][i + lane + 1] > sB[wid][i + lane];
-        npan_item += __popc(__ballot_sync(0xffffffffu, nonempty));
+        acc = fma(sPc[wid][pp] * wg, fma(lg, ib, ic), acc);
+      };
+      if (NL == 16) {  // the default N_l: lane l keeps node l mod 16; two independent
+                       // nodes per lane and pass (panels pp, pp + 2; pads weigh 0)
+        const double xg = sglx[lane & 15], wg = sglw[lane & 15];
+        for (int pp = lane >> 4; pp < nne; pp += 4) {
+          node(pp, xg, wg);
+          node(pp + 2, xg, wg);
+        }
+      } else {
+        const int nodes = nne * NL;
+        int pi = lane / NL, gq = lane - pi * NL;
+        for (int j = lane; j < nodes; j += 32, gq += 32) {
+          while (gq >= NL) { gq -= NL; ++pi; }
+          node(pi, sglx[gq], sglw[gq]);
+        }
       }
       __syncwarp();
     }
@@ -2483,6 +2563,7 @@ struct vp_ctx {
   int far_method = 0, fmm_p = 31, fmm_leaf = 40, fmm_levels = 0, tab_p = -1;
   int64_t fmm_outside = 0;
   int max_near_depth = 0;  // deepest near_eval leaf any element can produce (build_elements)
+  int psum_copies = 1;     // log-table copies of k_psum_tgt (VP_PSUM_COPIES: 1, 2, 4, 8)
   bool elems_ok = false;   // the last build_elements succeeded
   // multi-GPU (vp_multi.cuh): the library's NCCL communicator, if any
   void* comm = nullptr;
@@ -2493,13 +2574,13 @@ struct vp_ctx {
   int near_model = 0;
   double ball_factor = 1.5;
   int cache_max_depth = 3, cache_depth = -1;
-  int64_t cache_max_bytes = 12ll << 30;
+  int64_t cache_max_bytes = 0;  // 0: min(48 GiB, a quarter of the free device memory)
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
   DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
   DevBuf d_tl;  // per-target cached-leaf ranges (k_tgt_leafrange)
   DevBuf d_lsc, d_tover, d_ntover;  // list build: count-pass id scratch, overflow targets
   DevBuf d_neart;                   // per-target sums of the cached near leaves (evaluation)
-  int64_t leaf_scratch_budget = 4ll << 30;  // max bytes of the count pass's leaf scratch (VP_LEAF_SCRATCH_BYTES)
+  int64_t leaf_scratch_budget = 16ll << 30;  // max bytes of the count pass's leaf scratch (VP_LEAF_SCRATCH_BYTES)
   int tabs_p = -1;  // p of the density-independent tables (K1's V, near-cache Vt, SelfTab); -1: stale
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tk, f_tk2, f_tv, f_tord;  // FMM: target leaf keys and the leaf order of the targets
@@ -2895,7 +2976,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   CUDA_TRY(c, c->d_ldeep.ensure(sizeof(int32_t) * (n + 1)));
   // scratch for the first `cap` leaves of every pair (pairs with more are
   // walked again), within a budget: a quarter of the free device memory, at
-  // most leaf_scratch_budget (VP_LEAF_SCRATCH_BYTES, default 4 GiB) beyond
+  // most leaf_scratch_budget (VP_LEAF_SCRATCH_BYTES, default 16 GiB) beyond
   // what the context already holds; halved until the allocation succeeds
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
@@ -3013,10 +3094,22 @@ static void host_decode_path(unsigned long long path, int d, double v[6]) {
 // once per (p, rules, D), then contract on the device.
 // deepest cached level whose per-element cache fits the byte budget (-1: none)
 void decide_cache_depth(vp_ctx* c) {
+  // default budget: depth 3 for config 4 (1 M elements x 85 slots x 49 nodes
+  // = 35 GB) took the deep-leaf kernel 39.6 -> 12.6 ms and the pair stage
+  // 222 -> 214 ms against depth 2 within the former 12 GiB
+  int64_t budget = c->cache_max_bytes;
+  if (budget <= 0) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    budget = std::min<int64_t>(48ll << 30, (int64_t)(free_b / 4) + (int64_t)c->d_gcache.cap);
+  }
   int D = std::min(c->cache_max_depth, 6);
   while (D >= 0) {
     const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3;
-    if ((double)c->n_tri * nslot * c->rules.len_n * 8.0 <= (double)c->cache_max_bytes) break;
+    if ((double)c->n_tri * nslot * c->rules.len_n * 8.0 <= (double)budget) break;
     --D;
   }
   c->cache_depth = D;
@@ -3595,10 +3688,20 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   VP_DISPATCH_P(c->p, launch_self, c, T, nullptr, c->d_self.as<int32_t>(), txy, c->d_corr_self.as<double>(),
                 nullptr, nullptr);
   CUDA_TRY(c, cudaEventRecord(ev[9], c->s3));
-  k_psum_tgt<<<(unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64), PT_WARPS * 32, 0,
-               c->s3>>>(T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(),
-                        c->rules.len_q, c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(),
-                        c->d_psum.as<double>());
+  {
+    const unsigned pblocks = (unsigned)std::min<int64_t>(nblk(T, PT_WARPS), (int64_t)c->sm_count * 64);
+    auto psum_args = [&](auto kern, int copies) {
+      kern<<<pblocks, PT_WARPS * 32, sizeof(double2) * kLogEntries * copies, c->s3>>>(
+          T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), c->rules.len_q,
+          c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_psum.as<double>());
+    };
+    switch (c->psum_copies) {
+      case 2: psum_args(k_psum_tgt<2>, 2); break;
+      case 8: psum_args(k_psum_tgt<8>, 8); break;
+      case 4: psum_args(k_psum_tgt<4>, 4); break;
+      default: psum_args(k_psum_tgt<1>, 1); break;
+    }
+  }
   CUDA_TRY(c, cudaEventRecord(ev[8], c->s3));
   c->ss = c->stream;
   c->last_launches += 2;
@@ -3698,6 +3801,10 @@ int vp_create(int device, vp_ctx** out) {
   vp_ctx* c = new vp_ctx();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
+  if (const char* pc = std::getenv("VP_PSUM_COPIES")) c->psum_copies = std::atoi(pc);
+  // k_psum_tgt<8> takes 64 KB of dynamic shared memory
+  cudaFuncSetAttribute(k_psum_tgt<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(double2) * kLogEntries * 8));
   if (const char* lb = std::getenv("VP_LEAF_SCRATCH_BYTES")) {
     const long long v = std::atoll(lb);
     if (v > 0) c->leaf_scratch_budget = v;
@@ -3832,7 +3939,7 @@ int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
   if (max_depth < -1 || max_depth > 6) return set_err(c, 1, "set_near_cache: max_depth must be in [-1, 6]");
   if (max_bytes < 0) return set_err(c, 1, "set_near_cache: max_bytes must be >= 0");
   c->cache_max_depth = max_depth;
-  c->cache_max_bytes = max_bytes ? max_bytes : (12ll << 30);
+  c->cache_max_bytes = max_bytes;  // 0: min(48 GiB, free / 4)
   return 0;
 }
 

@@ -29,3 +29,10 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 print("\nby stall samples:")
 for d in sorted(data, key=lambda d: -d[1])[:n]:
     print(f"{d[1]:7d} {d[0]:>12,} {d[2][-5:]} {d[3]}")
+
+if len(sys.argv) > 3:  # full per-instruction list: offset from the function start
+    base = min(int(d[2], 16) for d in data)
+    with open(sys.argv[3], "w") as f:
+        f.write("offset,exec,samples,sass\n")
+        for d in data:
+            f.write(f"{int(d[2], 16) - base},{d[0]},{d[1]},\"{d[3]}\"\n")
