@@ -356,7 +356,11 @@ def main():
     if args.near_cache_gb or args.near_cache_depth != 3:
         ev.set_near_cache(args.near_cache_depth, int(args.near_cache_gb * (1 << 30)))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
-    stream = torch.cuda.current_stream(dev)
+    # a non-default stream: the library orders its work (and launches the
+    # captured graph) on the caller's stream, which the legacy default stream
+    # would not give it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     cfg = workload_config(args.config, pr.n_tri, pr.p, pr.q, pr.eps, args.seed, pr.n_tgt, S, stride,
                           0, world)
     out = {}
@@ -536,6 +540,16 @@ def main():
         if sfl:
             pstage["survey_flop_per_step"] = sfl
             pstage["survey_equiv_tflops"] = sfl / (pair_ms * 1e-3) / 1e12
+        # the same evaluation replayed from its captured CUDA graph (vp_evaluate_graph:
+        # no host round trip inside); replay time against the eager stage sum
+        gstep = lambda: ev.evaluate_graph(len(full), d_full.data_ptr(), d_uf.data_ptr(), stream.cuda_stream)  # noqa: E731
+        for _ in range(2):
+            gstep()
+        ev.graph_status(stream.cuda_stream)
+        g_ms, _, _ = timed_steps(gstep, n_p, stream, flush, dist, world)
+        ev.graph_status(stream.cuda_stream)
+        pstage["graph_ms_per_step"] = g_ms / n_p
+        pstage["eager_device_ms_per_step"] = float(np.mean([s["t_total_ms"] for s in p_st]))
         out["near_pair_integrals_per_s"] = pstage["near_pair_integrals_per_s"]
         out["pair_stage"] = pstage
 

@@ -134,6 +134,23 @@ int vp_evaluate(vp_ctx* ctx, int64_t n_tgt, const double* txy, double* u_out, vp
 int vp_evaluate_device(vp_ctx* ctx, int64_t n_tgt, const double* d_txy, double* d_u,
                        void* stream, vp_stats* st);
 
+/* Stream-ordered evaluation from a captured CUDA graph.  The first call for
+ * a (targets, output, configuration) triple runs one eager evaluation, which
+ * fixes every host-side size (list and leaf totals, overflow counts, FMM
+ * outside targets: they depend on the targets, mesh, rules and models, never
+ * on the density), then captures the same evaluation with no host round
+ * trip into a graph; every call launches that graph on `stream` (NULL: ctx
+ * stream) and returns at once.  The graph reads d_txy, the density
+ * coefficients and the rules in place: replays stay valid across
+ * vp_set_density of the same order, and are re-captured after any other
+ * vp_set_* or a different (n_tgt, d_txy, d_u).  The caller must not change
+ * the targets' values in place without a new pointer.  Errors of a replay
+ * and its counters: vp_graph_status. */
+int vp_evaluate_graph(vp_ctx* ctx, int64_t n_tgt, const double* d_txy, double* d_u, void* stream);
+/* Waits for `stream` (NULL: ctx stream) and reports the last replay's device
+ * error flags (status 2 as vp_evaluate) and counters (no device times). */
+int vp_graph_status(vp_ctx* ctx, void* stream, vp_stats* st);
+
 /* Far field only (fmm_eval --direct): u_far[t] =
  * sum_j q_j log r_tj^2, q_j = w_j |J| f_j / (4 pi); coincident pairs give 0. */
 int vp_far_field(vp_ctx* ctx, int64_t n_tgt, const double* txy, double* u_far);

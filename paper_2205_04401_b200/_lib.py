@@ -77,6 +77,9 @@ _SIGS = [
                                    ctypes.POINTER(VpStats)]),
     ("vp_evaluate_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(VpStats)]),
+    ("vp_evaluate_graph", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]),
+    ("vp_graph_status", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(VpStats)]),
     ("vp_far_field", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_double_p]),
     ("vp_sources", ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, c_double_p]),
     ("vp_near_pairs", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, c_double_p, c_int32_p,

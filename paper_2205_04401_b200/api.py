@@ -562,6 +562,17 @@ class Evaluator:
                self._err())
         return st.as_dict()
 
+    def evaluate_graph(self, n: int, d_txy: int, d_u: int, stream: int = 0):
+        """Launch the captured-graph evaluation (vp_evaluate_graph): async, no
+        host round trip after the first call for these buffers."""
+        _check(self._L.vp_evaluate_graph(self._h, n, ctypes.c_void_p(d_txy), ctypes.c_void_p(d_u),
+                                         ctypes.c_void_p(stream or None)), self._err())
+
+    def graph_status(self, stream: int = 0) -> dict:
+        st = VpStats()
+        _check(self._L.vp_graph_status(self._h, ctypes.c_void_p(stream or None), ctypes.byref(st)), self._err())
+        return st.as_dict()
+
     def far_field(self, txy):
         t = _f64(txy, (-1, 2))
         u = np.zeros(t.shape[0])

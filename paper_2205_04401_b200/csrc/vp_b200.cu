@@ -182,7 +182,7 @@ __global__ void k_cell_ranges(int64_t n, const int32_t* __restrict__ keys,
 // Candidates = the elements binned in t's cell merged with the all-near list.
 template <bool FILL>
 __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
-                        const ElemRec* __restrict__ el, GridDev g,
+                        const ElemRec* __restrict__ el, const float4* __restrict__ bbf, GridDev g,
                         const int64_t* __restrict__ cbeg, const int64_t* __restrict__ cend,
                         const int32_t* __restrict__ celems, const int32_t* __restrict__ allnear,
                         int n_allnear, int32_t* __restrict__ self_out,
@@ -224,8 +224,11 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
       id = ca;
       ++ia;
     }
+    // the element's near-field bbox rounded outward to float (all-near: the
+    // whole plane) rejects most candidates without touching the 192-B record
+    const float4 bb = bbf[id];
+    if (!(tx >= (double)bb.x && tx <= (double)bb.z && ty >= (double)bb.y && ty <= (double)bb.w)) continue;
     const ElemRec& R = el[id];
-    if ((R.ball != 0.0 || R.ta0 >= 0.0) && !(tx >= R.bx0 && tx <= R.bx1 && ty >= R.by0 && ty <= R.by1)) continue;
     if (self < 0) {
       double xi, eta;
       const int cid = curve_id_of(CV, id);
@@ -236,7 +239,7 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
         continue;
       }
     }
-    if (rn_in_near(R, tx, ty)) {
+    if (rn_in_near_fast(R, tx, ty)) {
       if (FILL) ids[o++] = id;
       else if (n < cap) scratch[t * cap + n] = id;
       ++n;
@@ -2541,7 +2544,7 @@ struct vp_ctx {
   RulesDev h_rd{};
   DevBuf d_rules;
   // elements
-  DevBuf d_el;
+  DevBuf d_el, d_bbf;  // element records; near-field bboxes rounded outward to float4
   std::vector<int32_t> h_allnear;
   DevBuf d_allnear;
   GridDev grid{};
@@ -2565,6 +2568,24 @@ struct vp_ctx {
   int max_near_depth = 0;  // deepest near_eval leaf any element can produce (build_elements)
   int psum_copies = 1;     // log-table copies of k_psum_tgt (VP_PSUM_COPIES: 1, 2, 4, 8)
   bool elems_ok = false;   // the last build_elements succeeded
+  // Evaluation plan: the host-side sizes an eager evaluation reads back
+  // (list and leaf totals, overflow counts, FMM outside targets).  They depend
+  // only on the targets, mesh, rules and models -- never on the density -- so
+  // a CUDA graph captured with them (vp_evaluate_graph) replays for any
+  // density of the same order with no host round trip.
+  struct Plan {
+    int64_t n_ids = 0, tot0 = 0, tot1 = 0, fmm_nout = 0;
+    unsigned list_nover = 0, leaf_nover = 0, ndeep = 0;
+    int leaf_cap = 1;
+  } plan;
+  bool capture = false;  // inside a stream capture: take sizes from `plan`, no host syncs
+  uint64_t gen = 1;      // bumped by every vp_set_* that changes the plan or the launch sequence
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t g_gen = 0;
+  int64_t g_n = -1;
+  const void *g_txy = nullptr, *g_u = nullptr;
+  unsigned long long* h_gstats = nullptr;  // pinned: stats + error flags of the last replay
   // multi-GPU (vp_multi.cuh): the library's NCCL communicator, if any
   void* comm = nullptr;
   int comm_world = 0, comm_rank = -1;
@@ -2750,6 +2771,29 @@ int build_elements(vp_ctx* c) {
   }
   CUDA_TRY(c, c->d_el.ensure(sizeof(ElemRec) * E));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_el.p, h.data(), sizeof(ElemRec) * E, cudaMemcpyHostToDevice, c->stream));
+  {
+    auto down = [](double x) {
+      float f = (float)x;
+      if ((double)f > x) f = std::nextafter(f, -INFINITY);
+      return f;
+    };
+    auto up = [](double x) {
+      float f = (float)x;
+      if ((double)f < x) f = std::nextafter(f, INFINITY);
+      return f;
+    };
+    std::vector<float4> bf(E);
+    for (int64_t e = 0; e < E; ++e) {
+      const ElemRec& R = h[e];
+      if (R.ball == 0.0 && R.ta0 < 0.0)
+        bf[e] = make_float4(-INFINITY, -INFINITY, INFINITY, INFINITY);  // all-near
+      else
+        bf[e] = make_float4(down(R.bx0), down(R.by0), up(R.bx1), up(R.by1));
+    }
+    CUDA_TRY(c, c->d_bbf.ensure(sizeof(float4) * E));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_bbf.p, bf.data(), sizeof(float4) * E, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
   CUDA_TRY(c, c->d_allnear.ensure(sizeof(int32_t) * (c->h_allnear.size() + 1)));
   if (!c->h_allnear.empty())
     CUDA_TRY(c, cudaMemcpyAsync(c->d_allnear.p, c->h_allnear.data(), sizeof(int32_t) * c->h_allnear.size(),
@@ -2978,19 +3022,26 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
   // walked again), within a budget: a quarter of the free device memory, at
   // most leaf_scratch_budget (VP_LEAF_SCRATCH_BYTES, default 16 GiB) beyond
   // what the context already holds; halved until the allocation succeeds
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-    cudaGetLastError();
-    free_b = 0;
-  }
-  int64_t budget = std::min<int64_t>(c->leaf_scratch_budget, (int64_t)(free_b / 4) + (int64_t)c->d_lscratch.cap);
-  int cap = 0;
+  int cap = c->plan.leaf_cap;
   for (;;) {
-    cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLeafScratchMax, (budget / 8) / std::max<int64_t>(n, 1)));
-    if (c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)) == cudaSuccess) break;
-    cudaGetLastError();
-    if (cap == 1) return set_err(c, 3, "near_eval: out of device memory for the leaf scratch");
-    budget /= 2;
+    if (c->capture) break;  // the eager run's cap; its scratch is allocated
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    static_cast<void>(total_b);
+    int64_t budget = std::min<int64_t>(c->leaf_scratch_budget, (int64_t)(free_b / 4) + (int64_t)c->d_lscratch.cap);
+    for (;;) {
+      cap = (int)std::max<int64_t>(1, std::min<int64_t>(kLeafScratchMax, (budget / 8) / std::max<int64_t>(n, 1)));
+      if (c->d_lscratch.ensure(sizeof(unsigned long long) * (size_t)std::max<int64_t>(n * cap, 1)) == cudaSuccess)
+        break;
+      cudaGetLastError();
+      if (cap == 1) return set_err(c, 3, "near_eval: out of device memory for the leaf scratch");
+      budget /= 2;
+    }
+    c->plan.leaf_cap = cap;
+    break;
   }
   CUDA_TRY(c, c->d_lover.ensure(sizeof(int32_t) * (n + 1)));
   CUDA_TRY(c, c->d_nover.ensure(2 * sizeof(unsigned)));
@@ -3013,12 +3064,23 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
                                 c->stream);
   int64_t tot[2] = {0, 0};
   unsigned nov[2] = {0, 0};
-  CUDA_TRY(c, cudaMemcpyAsync(&tot[0], c->d_loffc.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(&tot[1], c->d_loffd.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(nov, c->d_nover.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->capture) {
+    tot[0] = c->plan.tot0;
+    tot[1] = c->plan.tot1;
+    nov[0] = c->plan.leaf_nover;
+    nov[1] = c->plan.ndeep;
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(&tot[0], c->d_loffc.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&tot[1], c->d_loffd.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(nov, c->d_nover.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->plan.tot0 = tot[0];
+    c->plan.tot1 = tot[1];
+    c->plan.leaf_nover = nov[0];
+    c->plan.ndeep = nov[1];
+  }
   const int64_t nleaves = tot[0] + tot[1];
   const unsigned nover = nov[0], ndeep = nov[1];
   CUDA_TRY(c, c->d_leafc.ensure(sizeof(unsigned long long) * (tot[0] + 1)));
@@ -3094,6 +3156,7 @@ static void host_decode_path(unsigned long long path, int d, double v[6]) {
 // once per (p, rules, D), then contract on the device.
 // deepest cached level whose per-element cache fits the byte budget (-1: none)
 void decide_cache_depth(vp_ctx* c) {
+  if (c->capture) return;  // the eager run's depth
   // default budget: depth 3 for config 4 (1 M elements x 85 slots x 49 nodes
   // = 35 GB) took the deep-leaf kernel 39.6 -> 12.6 ms and the pair stage
   // 222 -> 214 ms against depth 2 within the former 12 GiB
@@ -3550,8 +3613,13 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   cub::DeviceSelect::Flagged(c->f_tmp.p, tmpb, it, c->f_flag.as<int32_t>(), c->f_oidx.as<int32_t>(),
                              c->f_cnt.as<int64_t>(), (int)T, c->fs);
   int64_t nout = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&nout, c->f_cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->fs));
-  CUDA_TRY(c, cudaStreamSynchronize(c->fs));
+  if (c->capture) {
+    nout = c->plan.fmm_nout;
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(&nout, c->f_cnt.p, sizeof(int64_t), cudaMemcpyDeviceToHost, c->fs));
+    CUDA_TRY(c, cudaStreamSynchronize(c->fs));
+    c->plan.fmm_nout = nout;
+  }
   c->fmm_outside = nout;
   if (nout > 0) {
     CUDA_TRY(c, c->f_otxy.ensure(sizeof(double2) * nout));
@@ -3581,7 +3649,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   const GridDev G = c->grid;
   const int nan = (int)c->h_allnear.size();
   k_lists<false><<<nblk(T, 128), 128, 0, c->stream>>>(
-      T, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
+      T, txy, c->d_el.as<ElemRec>(), c->d_bbf.as<float4>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
       c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c), nullptr,
       c->d_lsc.as<int32_t>(), cap, c->d_tover.as<int32_t>(), c->d_ntover.as<unsigned>(), c->d_err.as<int>() + 1);
@@ -3592,15 +3660,24 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   cub::DeviceScan::ExclusiveSum(c->d_tmp.p, tmpb, c->d_cnt.as<int64_t>(), c->d_off.as<int64_t>(), T + 1, c->stream);
   int64_t n_ids = 0;
   unsigned nover = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&n_ids, c->d_off.as<int64_t>() + T, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(&nover, c->d_ntover.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->capture) {
+    n_ids = c->plan.n_ids;
+    nover = c->plan.list_nover;
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(&n_ids, c->d_off.as<int64_t>() + T, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(&nover, c->d_ntover.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->plan.n_ids = n_ids;
+    c->plan.list_nover = nover;
+  }
   CUDA_TRY(c, c->d_ids.ensure(sizeof(int32_t) * (n_ids + 1)));
   k_lists_copy<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), cap, c->d_lsc.as<int32_t>(),
                                                     c->d_ids.as<int32_t>());
   if (nover > 0)
     k_lists<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
-        nover, txy, c->d_el.as<ElemRec>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
+        nover, txy, c->d_el.as<ElemRec>(), c->d_bbf.as<float4>(), G, c->d_cbeg.as<int64_t>(),
+        c->d_cend.as<int64_t>(),
         c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr, c->d_off.as<int64_t>(),
         c->d_ids.as<int32_t>(), nullptr, curves_dev(c), c->d_tover.as<int32_t>(), nullptr, 0, nullptr, nullptr,
         nullptr);
@@ -3654,7 +3731,12 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
       c->fs = c->stream;
     }
   } far_join{c, far_thread};
-  if (overlap) {
+  if (overlap && c->capture) {  // no host syncs inside: the far launches go inline on s2
+    CUDA_TRY(c, cudaStreamWaitEvent(c->s2, ev[6], 0));
+    c->fs = c->s2;
+    far_rc = far_sum(c, T, txy, c->d_ufar.as<double>(), false);
+    if (!far_rc) CUDA_TRY(c, cudaEventRecord(c->ev[2], c->s2));
+  } else if (overlap) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->s2, ev[6], 0));
     c->fs = c->s2;
     far_thread = std::thread([c, T, txy, &far_rc] {
@@ -3729,6 +3811,13 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
   c->last_launches += 2;
   CUDA_TRY(c, cudaEventRecord(ev[5], c->stream));
   CUDA_TRY(c, cudaGetLastError());
+  if (c->capture) {  // stats and error flags of every replay land in pinned memory
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_gstats, c->d_stats.p, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_gstats + 8, c->d_err.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    fork_guard.ok = true;
+    return 0;
+  }
   unsigned long long hs[8];
   int herr[2] = {0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(hs, c->d_stats.p, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
@@ -3913,11 +4002,15 @@ void vp_destroy(vp_ctx* c) {
   if (c->s3) cudaStreamDestroy(c->s3);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->comm) vp_comm_release(c);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->h_gstats) cudaFreeHost(c->h_gstats);
   delete c;
 }
 
 int vp_set_near_model(vp_ctx* c, int model, double ball_factor) {
   if (!c) return 1;
+  ++c->gen;
   if (model != 0 && model != 1) return set_err(c, 1, "set_near_model: model must be 0 (precise) or 1 (ball)");
   if (model == 1 && !(ball_factor >= 1.0)) return set_err(c, 1, "set_near_model: ball factor must be >= 1");
   c->near_model = model;
@@ -3936,6 +4029,7 @@ int vp_set_near_model(vp_ctx* c, int model, double ball_factor) {
 
 int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
   if (!c) return 1;
+  ++c->gen;
   if (max_depth < -1 || max_depth > 6) return set_err(c, 1, "set_near_cache: max_depth must be in [-1, 6]");
   if (max_bytes < 0) return set_err(c, 1, "set_near_cache: max_bytes must be >= 0");
   c->cache_max_depth = max_depth;
@@ -3945,6 +4039,7 @@ int vp_set_near_cache(vp_ctx* c, int max_depth, int64_t max_bytes) {
 
 int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
   if (!c) return 1;
+  ++c->gen;
   if (method < 0 || method > 2)
     return set_err(c, 1, "set_far_method: method must be 0 (direct), 1 (fmm) or 2 (none: corrections only)");
   if (order != 0 && (order < 4 || order > kFmmMaxP))
@@ -3968,6 +4063,7 @@ int vp_device_info(vp_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {
 
 int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri) {
   if (!c) return 1;
+  ++c->gen;
   if (n_vert <= 0 || n_tri <= 0 || !vxy || !tri)
     return set_err(c, 1, "set_mesh: empty mesh (invariant: n_vert > 0, n_tri > 0)");
   if (n_tri > (int64_t)INT32_MAX / 4) return set_err(c, 1, "set_mesh: too many triangles");
@@ -4013,6 +4109,7 @@ int vp_set_mesh(vp_ctx* c, int64_t n_vert, const double* vxy, int64_t n_tri, con
 int vp_set_curves(vp_ctx* c, const int32_t* curve_id, int deg, int64_t n_curves, const double* cx,
                   const double* cy, const double* len) {
   if (!c) return 1;
+  ++c->gen;
   if (!c->have_mesh) return set_err(c, 1, "set_curves: call vp_set_mesh first");
   c->h_ecurve.clear();
   c->h_celist.clear();
@@ -4065,6 +4162,7 @@ int vp_set_curves(vp_ctx* c, const int32_t* curve_id, int deg, int64_t n_curves,
 
 int vp_set_rules(vp_ctx* c, const vp_rules* r) {
   if (!c) return 1;
+  ++c->gen;
   if (!r) return set_err(c, 1, "set_rules: null rules");
   if (r->len_q <= 0 || r->len_q > kMaxFar || !r->far_x || !r->far_y || !r->far_w)
     return set_err(c, 1, "set_rules: far rule length must be in [1, 1024]");
@@ -4135,6 +4233,7 @@ int vp_set_density(vp_ctx* c, int p, const double* coeffs) {
   if (!coeffs) return set_err(c, 1, "set_density: null coefficients");
   const int M = koorn_size(p);
   CUDA_TRY(c, cudaSetDevice(c->device));
+  if (p != c->p || c->d_coeffs.cap < sizeof(double) * c->n_tri * M) ++c->gen;  // a captured graph reads d_coeffs
   CUDA_TRY(c, c->d_coeffs.ensure(sizeof(double) * c->n_tri * M));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_coeffs.p, coeffs, sizeof(double) * c->n_tri * M, cudaMemcpyHostToDevice, c->stream));
   c->p = p;
@@ -4210,6 +4309,77 @@ int vp_evaluate_device(vp_ctx* c, int64_t n_tgt, const double* d_txy, double* d_
   }
   const int rc = evaluate_impl(c, n_tgt, (const double2*)d_txy, d_u, st);
   return rc;
+}
+
+int vp_evaluate_graph(vp_ctx* c, int64_t n_tgt, const double* d_txy, double* d_u, void* stream) {
+  if (int rc = ensure_ready(c, true)) return rc;
+  if (n_tgt <= 0 || !d_txy || !d_u) return set_err(c, 1, "evaluate_graph: need n_tgt > 0 and device arrays");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaStream_t user = stream ? (cudaStream_t)stream : c->stream;
+  const bool fresh = c->gexec && c->g_gen == c->gen && c->g_n == n_tgt && c->g_txy == d_txy && c->g_u == d_u;
+  if (!fresh) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->graph) cudaGraphDestroy(c->graph);
+    c->gexec = nullptr;
+    c->graph = nullptr;
+    if (!c->h_gstats) CUDA_TRY(c, cudaMallocHost(&c->h_gstats, sizeof(unsigned long long) * 16));
+    // eager evaluation on the ctx stream: fills the plan and every buffer
+    if (user != c->stream) {
+      cudaEvent_t e;
+      CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      cudaEventRecord(e, user);
+      cudaStreamWaitEvent(c->stream, e, 0);
+      cudaEventDestroy(e);
+    }
+    if (int rc = evaluate_impl(c, n_tgt, (const double2*)d_txy, d_u, nullptr)) return rc;
+    // capture the same evaluation with the plan's sizes
+    CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capture = true;
+    const int rc = evaluate_impl(c, n_tgt, (const double2*)d_txy, d_u, nullptr);
+    c->capture = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return set_err(c, 3, std::string("cuda: capture failed: ") + cudaGetErrorString(ce));
+    CUDA_TRY(c, cudaGraphInstantiate(&c->gexec, g, 0));
+    c->graph = g;
+    c->g_gen = c->gen;
+    c->g_n = n_tgt;
+    c->g_txy = d_txy;
+    c->g_u = d_u;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  CUDA_TRY(c, cudaGraphLaunch(c->gexec, user));
+  return 0;
+}
+
+int vp_graph_status(vp_ctx* c, void* stream, vp_stats* st) {
+  if (!c) return 1;
+  if (!c->gexec) return set_err(c, 1, "graph_status: no captured evaluation");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(stream ? (cudaStream_t)stream : c->stream));
+  const unsigned long long* hs = c->h_gstats;
+  const int* herr = reinterpret_cast<const int*>(hs + 8);
+  if (herr[1]) return set_err(c, 2, "evaluate: non-finite target coordinate");
+  if (herr[0]) return set_err(c, 2, "near_eval: subdivision exceeded depth/frontier limits");
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->n_targets = c->g_n;
+    st->n_near_pairs = c->plan.n_ids;
+    st->n_leaves = c->plan.tot0 + c->plan.tot1 + (int64_t)hs[6];
+    st->n_rho_le1 = (int64_t)hs[1];
+    st->max_depth = (int32_t)hs[2];
+    st->n_panels = (int64_t)hs[3];
+    st->n_degenerate = (int64_t)hs[4];
+    st->n_self = (int64_t)hs[5];
+    st->n_outside = c->g_n - st->n_self;
+    st->n_sources = c->n_tri * c->rules.len_q;
+    st->far_method = c->far_method;
+  }
+  return 0;
 }
 
 int vp_evaluate(vp_ctx* c, int64_t n_tgt, const double* txy, double* u_out, vp_stats* st) {

@@ -85,6 +85,36 @@ __device__ __forceinline__ bool rn_in_near(const ElemRec& E, double tx, double t
   return (rn_add(d0, d1) < E.ta0) || (rn_add(d1, d2) < E.ta1) || (rn_add(d2, d0) < E.ta2);
 }
 
+// rn_in_near's decision from float square roots where it is clear by a
+// 4e-7 relative margin, the exactly rounded test otherwise: the decisions are
+// bit-identical.  (s_k = fl32(sqrt(fl32(r_k^2))) is within 1e-7 of the exact
+// distance, so s_0 + s_1 is within 1e-7 of the exact left-hand side.)
+__device__ __forceinline__ bool rn_in_near_fast(const ElemRec& E, double tx, double ty) {
+  if (E.ball != 0.0 || E.ta0 < 0.0) return rn_in_near(E, tx, ty);
+  const double px[3] = {E.x0, E.x1, E.x2}, py[3] = {E.y0, E.y1, E.y2};
+  double s[3];
+  bool range_ok = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double dx = tx - px[k], dy = ty - py[k];
+    const double r2 = fma(dx, dx, dy * dy);
+    range_ok = range_ok && r2 > 1e-30 && r2 < 1e30;
+    s[k] = (double)__fsqrt_rn((float)r2);
+  }
+  if (range_ok) {
+    const double ta[3] = {E.ta0, E.ta1, E.ta2};
+    bool ambiguous = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double l = s[k] + s[(k + 1) % 3];
+      if (l < ta[k] * (1.0 - 4e-7)) return true;
+      ambiguous = ambiguous || !(l > ta[k] * (1.0 + 4e-7));
+    }
+    if (!ambiguous) return false;
+  }
+  return rn_in_near(E, tx, ty);
+}
+
 // ---------------------------------------------------------------------------
 // compile-time Koornwinder recurrence coefficients
 __host__ __device__ constexpr double kc_la(int m) { return double(2 * m + 1) / double(m + 1); }

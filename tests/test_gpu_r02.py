@@ -176,3 +176,32 @@ def test_comm_world1_gather_and_stats():
         for k in ("n_targets", "n_near_pairs", "n_leaves", "n_panels"):
             assert st2[k] == st[k]
         assert abs(st2["t_total_ms"] - st["t_total_ms"]) < 1e-9
+
+
+@pytest.mark.parametrize("far", ["direct", "fmm", "none"])
+def test_graph_replay_matches_eager(far):
+    """vp_evaluate_graph: the captured evaluation (no host round trips)
+    reproduces the eager one bit for bit, also after vp_set_density with new
+    coefficients of the same order, and vp_graph_status reports its counters."""
+    import torch
+    pr = vp.load_config(2)
+    t = np.ascontiguousarray(pr.txy[::5])
+    with vp.Evaluator(0) as ev:
+        ev.load(pr)
+        ev.set_far_method(far)
+        u_e, st_e = ev.evaluate(t)
+        d_t = torch.from_numpy(t).cuda()
+        d_u = torch.zeros(len(t), dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        for _ in range(3):
+            ev.evaluate_graph(len(t), d_t.data_ptr(), d_u.data_ptr(), s.cuda_stream)
+        st_g = ev.graph_status(s.cuda_stream)
+        assert np.array_equal(d_u.cpu().numpy(), u_e)
+        for k in ("n_near_pairs", "n_leaves", "n_panels", "n_self", "n_rho_le1", "max_depth"):
+            assert st_g[k] == st_e[k], k
+        c2 = pr.coeffs * 0.5 + 0.25 * np.roll(pr.coeffs, 7, axis=0)
+        ev.set_density(pr.p, c2)
+        u_e2, _ = ev.evaluate(t)
+        ev.evaluate_graph(len(t), d_t.data_ptr(), d_u.data_ptr(), s.cuda_stream)
+        ev.graph_status(s.cuda_stream)
+        assert np.array_equal(d_u.cpu().numpy(), u_e2)
