@@ -180,8 +180,11 @@ __global__ void k_cell_ranges(int64_t n, const int32_t* __restrict__ keys,
 // ---------------------------------------------------------------------------
 // K3: S(t) (lowest containing id) and N(t) (ascending) for every target.
 // Candidates = the elements binned in t's cell merged with the all-near list.
-template <bool FILL>
-__global__ void k_lists(int64_t T, const double2* __restrict__ txy,
+// CURVED: the mesh has curved elements (their Newton locate is inlined only
+// then; straight meshes run at 4 -> 8 resident blocks with 124 -> <= 64 registers)
+template <bool FILL, bool CURVED>
+__global__ void __launch_bounds__(128, CURVED ? 1 : 8)
+    k_lists(int64_t T, const double2* __restrict__ txy,
                         const ElemRec* __restrict__ el, const float4* __restrict__ bbf, GridDev g,
                         const int64_t* __restrict__ cbeg, const int64_t* __restrict__ cend,
                         const int32_t* __restrict__ celems, const int32_t* __restrict__ allnear,
@@ -231,7 +234,7 @@ __global__ void k_lists(int64_t T, const double2* __restrict__ txy,
     const ElemRec& R = el[id];
     if (self < 0) {
       double xi, eta;
-      const int cid = curve_id_of(CV, id);
+      const int cid = CURVED ? curve_id_of(CV, id) : -1;
       if (cid < 0 ? rn_locate(R, tx, ty, xi, eta) : rn_locate_curved(R, curve_of(CV, cid), tx, ty, xi, eta)) {
         self = id;
         sxi = xi;
@@ -942,8 +945,12 @@ __global__ void __launch_bounds__(128)
   const int SA = nc_stride(Kp), SB = nc_stride(kNcBN);
   double* As = ncs;                 // [kNcBM][SA]
   double* Bs = ncs + kNcBM * SA;    // [Kp][SB]
-  const int64_t e0 = (int64_t)blockIdx.x * kNcBM;
-  const int64_t r0 = (int64_t)blockIdx.y * kNcBN;
+  // 1-D grid, row block fastest: the blocks of one element block run back to
+  // back and share its coefficients in L2 (element block fastest re-read all
+  // 235 MB of config 4's coefficients once per row block: 28 GB of DRAM reads)
+  const int64_t nrb = (R + kNcBN - 1) / kNcBN;
+  const int64_t e0 = ((int64_t)blockIdx.x / nrb) * kNcBM;
+  const int64_t r0 = ((int64_t)blockIdx.x % nrb) * kNcBN;
   __shared__ double sdet[kNcBM];
   if (threadIdx.x < kNcBM) sdet[threadIdx.x] = e0 + threadIdx.x < E ? el[e0 + threadIdx.x].det : 0.0;
   __syncthreads();
@@ -3222,9 +3229,9 @@ int build_near_cache(vp_ctx* c) {
   CUDA_TRY(c, cudaMemsetAsync(c->d_gcache.as<double>() + c->n_tri * R, 0, sizeof(double) * (Ln + 64), c->stream));
   static const bool cache_simt = getenv("VP_NEAR_CACHE_SIMT") != nullptr;  // A/B switch: DFMA kernel
   if (!cache_simt) {
-    if (nblk(R, kNcBN) > 65535u) return set_err(c, 1, "near cache: too many rows");
-    dim3 grid((unsigned)((c->n_tri + kNcBM - 1) / kNcBM), (unsigned)nblk(R, kNcBN));
-    k_near_cache_mma<<<grid, 128, near_cache_mma_smem(M), c->stream>>>(
+    const int64_t nb = (int64_t)((c->n_tri + kNcBM - 1) / kNcBM) * nblk(R, kNcBN);
+    if (nb > (int64_t)INT32_MAX) return set_err(c, 1, "near cache: too many blocks");
+    k_near_cache_mma<<<(unsigned)nb, 128, near_cache_mma_smem(M), c->stream>>>(
         c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(), c->d_el.as<ElemRec>(),
         c->d_gcache.as<double>());
   } else {
@@ -3648,7 +3655,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   CUDA_TRY(c, cudaMemsetAsync(c->d_ntover.p, 0, sizeof(unsigned), c->stream));
   const GridDev G = c->grid;
   const int nan = (int)c->h_allnear.size();
-  k_lists<false><<<nblk(T, 128), 128, 0, c->stream>>>(
+  (has_curves(c) ? k_lists<false, true> : k_lists<false, false>)<<<nblk(T, 128), 128, 0, c->stream>>>(
       T, txy, c->d_el.as<ElemRec>(), c->d_bbf.as<float4>(), G, c->d_cbeg.as<int64_t>(), c->d_cend.as<int64_t>(),
       c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, c->d_self.as<int32_t>(),
       c->d_cnt.as<int64_t>(), nullptr, nullptr, c->d_selfref.as<double2>(), curves_dev(c), nullptr,
@@ -3675,7 +3682,7 @@ int build_lists(vp_ctx* c, int64_t T, const double2* txy, int64_t* n_ids_out) {
   k_lists_copy<<<nblk(T, 256), 256, 0, c->stream>>>(T, c->d_off.as<int64_t>(), cap, c->d_lsc.as<int32_t>(),
                                                     c->d_ids.as<int32_t>());
   if (nover > 0)
-    k_lists<true><<<nblk(nover, 128), 128, 0, c->stream>>>(
+    (has_curves(c) ? k_lists<true, true> : k_lists<true, false>)<<<nblk(nover, 128), 128, 0, c->stream>>>(
         nover, txy, c->d_el.as<ElemRec>(), c->d_bbf.as<float4>(), G, c->d_cbeg.as<int64_t>(),
         c->d_cend.as<int64_t>(),
         c->d_celems.as<int32_t>(), c->d_allnear.as<int32_t>(), nan, nullptr, nullptr, c->d_off.as<int64_t>(),
