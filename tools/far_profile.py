@@ -31,8 +31,13 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
-    h, v = r[0], r[2]
-    g = lambda k: float(v[h.index(k)].replace(",", ""))  # noqa: E731
+    h, units, v = r[0], r[1], r[2]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-6,
+             "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+
+    def g(k):  # value in bytes, or in ms for durations
+        i = h.index(k)
+        return float(v[i].replace(",", "")) * scale.get(units[i], 1.0)
     T = bj["counts"]["targets_per_gpu"]
     S = bj["config"]["sources"]
     fl = 2 * g(EXTRA[0]) + g(EXTRA[1]) + g(EXTRA[2])
@@ -42,7 +47,7 @@ def main():
            "dram_bytes_read": g("dram__bytes_read.sum"), "dram_bytes_write": g("dram__bytes_write.sum"),
            "dram_bytes_per_launch": g("dram__bytes_read.sum") + g("dram__bytes_write.sum"),
            "fp64_flops": fl, "flop_per_pair_ncu": fl / (T * S),
-           "duration_ms": g("gpu__time_duration.sum") * (1e-6 if h and "nsecond" in r[1][h.index("gpu__time_duration.sum")] else 1e-3),
+           "duration_ms": g("gpu__time_duration.sum"),
            "fp64_pipe_active_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")}
     json.dump(doc, open(out, "w"), indent=1)
     print(json.dumps(doc))
