@@ -11,9 +11,10 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xptxas -v 
 CXXFLAGS := -O2 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(CSRC)
 
 LIB := $(PKG)/libvp_b200.so
+ABI_CALLER := tests/cpp/vp_abi_caller
 OBJS := $(CSRC)/vp_b200.o $(CSRC)/vp_setup.o $(CSRC)/vp_curves.o
 
-all: $(LIB) oracle
+all: $(LIB) oracle $(ABI_CALLER)
 
 $(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/vp_curve.cuh $(CSRC)/vp_fmm.cuh $(CSRC)/vp_multi.cuh \
 		$(CSRC)/koorn.cuh include/vp.h include/vp_setup.h
@@ -28,6 +29,12 @@ $(CSRC)/vp_curves.o: $(CSRC)/vp_curves.cpp include/vp_setup.h
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(OBJS) -lpthread -ldl
 
+# a plain C++ caller of the C-ABI (no Python): tests/test_abi.py, tests/test_gpu_r02.py
+$(ABI_CALLER): tests/cpp/vp_abi_caller.cpp include/vp.h include/vp_setup.h $(LIB)
+	$(CXX) -O2 -std=c++17 -Wall -Wextra -Iinclude -o $@ $< -L$(PKG) -lvp_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+abi-caller: $(ABI_CALLER)
+
 oracle:
 	$(MAKE) -C oracle
 
@@ -35,7 +42,7 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(OBJS) $(LIB) $(CSRC)/ptxas.log
+	rm -f $(OBJS) $(LIB) $(CSRC)/ptxas.log $(ABI_CALLER)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref clean abi-caller

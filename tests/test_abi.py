@@ -129,3 +129,18 @@ def test_ctypes_structs_mirror_headers(header, name, cls):
     header's order (a field added on one side only shifts every later one)."""
     fields = [f for f, _ in getattr(_lib, cls)._fields_]
     assert fields == header_struct_fields(header, name)
+
+
+def test_cpp_caller_builds_and_refuses_without_device():
+    """A plain C++ program links libvp_b200.so through include/*.h only
+    (tests/cpp/vp_abi_caller.cpp, the reference-side binding of INTEGRATION.md);
+    without a GPU it stops with status 3 (no CPU fallback)."""
+    import subprocess
+    r = subprocess.run(["make", "-C", ROOT, "abi-caller"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    exe = os.path.join(ROOT, "tests", "cpp", "vp_abi_caller")
+    assert os.path.exists(exe)
+    if _has_gpu():
+        pytest.skip("a GPU is present (run by tests/test_gpu_r02.py)")
+    r = subprocess.run([exe, "/tmp/vp_abi_caller_u.bin"], capture_output=True, text=True)
+    assert r.returncode == 3, (r.returncode, r.stderr)

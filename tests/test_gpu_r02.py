@@ -205,3 +205,23 @@ def test_graph_replay_matches_eager(far):
         ev.evaluate_graph(len(t), d_t.data_ptr(), d_u.data_ptr(), s.cuda_stream)
         ev.graph_status(s.cuda_stream)
         assert np.array_equal(d_u.cpu().numpy(), u_e2)
+
+
+def test_cpp_caller_on_gpu(tmp_path):
+    """The C++ caller (no Python in the process): config 1 through vp.h, the
+    two vp_shard_plan shards bitwise equal to the one-shot u, u within 1e-11
+    of the oracle."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", root, "abi-caller"], check=True, capture_output=True)
+    out = str(tmp_path / "u.bin")
+    r = subprocess.run([os.path.join(root, "tests", "cpp", "vp_abi_caller"), out, "1"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "bitwise equal" in r.stdout
+    u = np.fromfile(out, dtype=np.float64)
+    pr = vp.load_config(1)
+    assert u.size == pr.n_tgt
+    u_o, _, _ = Oracle.from_problem(pr).evaluate(pr.txy[::3])
+    assert rel(u[::3], u_o) <= REL_TOL
