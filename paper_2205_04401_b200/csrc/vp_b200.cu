@@ -1823,8 +1823,8 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
   __shared__ double sF[SELF_WARPS][M3], sE[SELF_WARPS][3][2 * NP];
   // non-empty panels of the side in progress: sl = a + b x_gl (panel middle and
   // half width over L), weight h (half width) w_gl
-  __shared__ double sPa[SELF_WARPS][kMaxSelfPanels + 4], sPb[SELF_WARPS][kMaxSelfPanels + 4],
-      sPc[SELF_WARPS][kMaxSelfPanels + 4];
+  __shared__ double sPa[SELF_WARPS][kMaxSelfPanels + 8], sPb[SELF_WARPS][kMaxSelfPanels + 8],
+      sPc[SELF_WARPS][kMaxSelfPanels + 8];
   __shared__ SelfSide sS[SELF_WARPS][3];
   constexpr bool kHorner = P <= kSelfHornerMaxP;
   extern __shared__ __align__(16) double sT2[];  // [2 NP][M], dynamic
@@ -1974,7 +1974,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         nne += __popc(bal);
       }
       npan_item += nne;
-      if (lane < 4) {  // zero-weight pad panels: the paired node loop needs no bound test
+      if (lane < 8) {  // zero-weight pad panels: the grouped node loop needs no bound test
         sPa[wid][nne + lane] = 0.0;
         sPb[wid][nne + lane] = 0.0;
         sPc[wid][nne + lane] = 0.0;
@@ -2023,9 +2023,12 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       if (NL == 16) {  // the default N_l: lane l keeps node l mod 16; two independent
                        // nodes per lane and pass (panels pp, pp + 2; pads weigh 0)
         const double xg = sglx[lane & 15], wg = sglw[lane & 15];
-        for (int pp = lane >> 4; pp < nne; pp += 4) {
-          node(pp, xg, wg);
-          node(pp + 2, xg, wg);
+#ifndef VP_SELF_NODES
+#define VP_SELF_NODES 2
+#endif
+        for (int pp = lane >> 4; pp < nne; pp += 2 * VP_SELF_NODES) {
+#pragma unroll
+          for (int u = 0; u < VP_SELF_NODES; ++u) node(pp + 2 * u, xg, wg);
         }
       } else {
         const int nodes = nne * NL;
