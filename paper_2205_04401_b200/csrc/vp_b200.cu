@@ -935,11 +935,18 @@ __global__ void __launch_bounds__(256)
 // = 4 (mod 16) doubles so the m8n8k4 fragment loads are conflict-free; each
 // of the 4 warps owns 32 x 16 outputs (4 x 2 DMMA tiles, 16 accumulators).
 // K = M padded to a multiple of 4 with zeros.
+// elements some pair of this call refers to (the cache is built for them only:
+// a rank's shard of a sharded job, the per-pair API's few pairs)
+__global__ void k_mark_elems(int64_t n, const int32_t* __restrict__ pelem, uint8_t* __restrict__ used) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) used[pelem[i]] = 1;
+}
+
 constexpr int kNcBM = 32, kNcBN = 64;
 __host__ __device__ constexpr int nc_stride(int k) { return k + ((4 - k % 16) + 16) % 16; }
 __global__ void __launch_bounds__(128)
     k_near_cache_mma(int64_t E, int M, int64_t R, const double* __restrict__ Vt, const double* __restrict__ coeffs,
-                     const ElemRec* __restrict__ el, double* __restrict__ out) {
+                     const ElemRec* __restrict__ el, double* __restrict__ out, const uint8_t* __restrict__ used) {
   extern __shared__ __align__(16) double ncs[];
   const int Kp = (M + 3) & ~3;
   const int SA = nc_stride(Kp), SB = nc_stride(kNcBN);
@@ -951,6 +958,10 @@ __global__ void __launch_bounds__(128)
   const int64_t nrb = (R + kNcBN - 1) / kNcBN;
   const int64_t e0 = ((int64_t)blockIdx.x / nrb) * kNcBM;
   const int64_t r0 = ((int64_t)blockIdx.x % nrb) * kNcBN;
+  if (used) {  // an element block no pair of the call refers to: nothing to build
+    const bool mine = threadIdx.x < kNcBM && e0 + threadIdx.x < E && used[e0 + threadIdx.x];
+    if (!__syncthreads_or(mine)) return;
+  }
   __shared__ double sdet[kNcBM];
   if (threadIdx.x < kNcBM) sdet[threadIdx.x] = e0 + threadIdx.x < E ? el[e0 + threadIdx.x].det : 0.0;
   __syncthreads();
@@ -2606,6 +2617,7 @@ struct vp_ctx {
   double ball_factor = 1.5;
   int cache_max_depth = 3, cache_depth = -1;
   int64_t cache_max_bytes = 0;  // 0: min(48 GiB, a quarter of the free device memory)
+  DevBuf d_elused;  // near cache: elements referred to by the call's pairs
   DevBuf d_cacheV, d_gcache, d_npa, d_npb, d_nps, d_slotref, d_psum, d_lscratch, d_lover, d_nover;
   DevBuf d_lcntc, d_lcntd, d_loffc, d_loffd, d_leafc, d_leafd, d_ldeep;  // leaves split at the cache depth
   DevBuf d_tl;  // per-target cached-leaf ranges (k_tgt_leafrange)
@@ -3014,7 +3026,7 @@ void launch_near_curved(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t
       c->d_stats.as<unsigned long long>(), c->d_err.as<int>());
 }
 
-int build_near_cache(vp_ctx* c);
+int build_near_cache(vp_ctx* c, const int32_t* pelem, int64_t n_pairs);
 void decide_cache_depth(vp_ctx* c);
 
 // T/toff: the evaluation's targets and pair CSR (cached leaves then summed per
@@ -3105,7 +3117,7 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
         nover, ptgt, pelem, txy, c->d_el.as<ElemRec>(), c->d_rules.as<RulesDev>(), nullptr, lo,
         c->d_stats.as<unsigned long long>(), c->d_err.as<int>(), curves_dev(c), c->d_lover.as<int32_t>(), nullptr, 0,
         nullptr, nullptr, 32);
-  if (int rc = build_near_cache(c)) return rc;
+  if (int rc = build_near_cache(c, pelem, n)) return rc;
   CUDA_TRY(c, c->d_npa.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_npb.ensure(sizeof(double) * (n + 1)));
   CUDA_TRY(c, c->d_nps.ensure(sizeof(double) * (n + 1)));
@@ -3188,10 +3200,19 @@ void decide_cache_depth(vp_ctx* c) {
   c->cache_depth = D;
 }
 
-int build_near_cache(vp_ctx* c) {
+int build_near_cache(vp_ctx* c, const int32_t* pelem, int64_t n_pairs) {
   const int Ln = c->rules.len_n, M = c->M;
   const int D = c->cache_depth;
   if (D < 0) return 0;
+  // element flags of the call's pairs; only their cache rows are built
+  const uint8_t* used = nullptr;
+  if (pelem && n_pairs > 0) {
+    CUDA_TRY(c, c->d_elused.ensure((size_t)c->n_tri + 1));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_elused.p, 0, (size_t)c->n_tri, c->stream));
+    k_mark_elems<<<nblk(n_pairs, 256), 256, 0, c->stream>>>(n_pairs, pelem, c->d_elused.as<uint8_t>());
+    used = c->d_elused.as<uint8_t>();
+    c->last_launches += 1;
+  }
   const int64_t nslot = ((1ll << (2 * (D + 1))) - 1) / 3, R = nslot * Ln;
   if (c->cacheV_depth != D || c->cacheV_p != c->p) {
     std::vector<double> Vt((size_t)M * R), kv(M), sref(6 * nslot);
@@ -3236,7 +3257,7 @@ int build_near_cache(vp_ctx* c) {
     if (nb > (int64_t)INT32_MAX) return set_err(c, 1, "near cache: too many blocks");
     k_near_cache_mma<<<(unsigned)nb, 128, near_cache_mma_smem(M), c->stream>>>(
         c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(), c->d_el.as<ElemRec>(),
-        c->d_gcache.as<double>());
+        c->d_gcache.as<double>(), used);
   } else {
     if (nblk(R, 256) > 65535u) return set_err(c, 1, "near cache: too many rows");
     dim3 grid((unsigned)((c->n_tri + kCacheNE - 1) / kCacheNE), (unsigned)nblk(R, 256));
