@@ -362,7 +362,7 @@ __device__ __forceinline__ double far_log_k2(const double2* tab, unsigned laneof
   }
 }
 
-template <bool ZERO_CHECK>
+template <bool ZERO_CHECK, int R = FAR_R>
 __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
     k_far(int64_t T, const double2* __restrict__ txy, int64_t S, const double* __restrict__ sx,
           const double* __restrict__ sy, const double* __restrict__ sq, int64_t chunk,
@@ -373,10 +373,10 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
   double* ssq = reinterpret_cast<double*>(sxy + FAR_TILE);
   for (int i = threadIdx.x; i < kFarLogEntries * kFarCopies; i += FAR_THREADS) tab[i] = g_fartab[i / kFarCopies];
   const unsigned laneoff = 16u * (threadIdx.x & (kFarCopies - 1));
-  const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * FAR_R) + threadIdx.x;
-  double tx[FAR_R], ty[FAR_R], acc[FAR_R];
+  const int64_t tb = (int64_t)blockIdx.x * (FAR_THREADS * R) + threadIdx.x;
+  double tx[R], ty[R], acc[R];
 #pragma unroll
-  for (int r = 0; r < FAR_R; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int64_t t = tb + (int64_t)r * FAR_THREADS;
     const double2 p = t < T ? txy[t] : make_double2(0.0, 0.0);
     tx[r] = p.x;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
       const double2 ps = sxy[j];
       const double q = ssq[j];
 #pragma unroll
-      for (int r = 0; r < FAR_R; ++r) {
+      for (int r = 0; r < R; ++r) {
         const double dx = tx[r] - ps.x, dy = ty[r] - ps.y;
         const double r2 = fma(dx, dx, dy * dy);
         acc[r] = fma(q, far_log_k2<ZERO_CHECK>(tab, laneoff, c3ff, r2), acc[r]);
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(FAR_THREADS, VP_FAR_MINB)
     }
   }
 #pragma unroll
-  for (int r = 0; r < FAR_R; ++r) {
+  for (int r = 0; r < R; ++r) {
     const int64_t t = tb + (int64_t)r * FAR_THREADS;
     if (t < T) part[(int64_t)blockIdx.y * T + t] = acc[r];
   }
@@ -3507,22 +3507,31 @@ int direct_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool 
   int64_t chunk = std::max<int64_t>(4096, (S + 255) / 256);
   chunk = (chunk + FAR_TILE - 1) / FAR_TILE * FAR_TILE;
   const int nsplit = (int)std::max<int64_t>(1, (S + chunk - 1) / chunk);
+  // Targets per thread: 8 (the fastest per pair), or 4 when a target count
+  // that is not a multiple of 4,096 would leave the last block of 8-target
+  // threads mostly idle (one block per SM, so a block is the unit of time):
+  // the cost model is waves x targets per block x per-pair speed (4-target
+  // threads measured ~3 % slower per pair).  A strong-scaled shard of the
+  // config-4 subset at 8 GPUs (14,336 targets = 3.5 x 4,096) takes 4.  Each
+  // target's sum is the same fixed-order sum either way (bitwise invariant).
+  auto cost = [&](int r) {
+    const int64_t tb = (int64_t)FAR_THREADS * r;
+    const double waves = std::ceil((double)nblk(T, (int)tb) * nsplit / (double)c->sm_count);
+    return waves * (double)tb * (r == 4 ? 1.03 : 1.0);
+  };
+  static const int forced = std::getenv("VP_FAR_TPT") ? std::atoi(std::getenv("VP_FAR_TPT")) : 0;  // A/B: 4 or 8
+  const int R = forced == 4 || forced == 8 ? (forced == 4 ? 4 : FAR_R) : (FAR_R == 8 && cost(4) < cost(8)) ? 4 : FAR_R;
   // targets in batches so the [nsplit x batch] partials stay within 1 GiB
-  const int64_t tblk = (int64_t)FAR_THREADS * FAR_R;
+  const int64_t tblk = (int64_t)FAR_THREADS * R;
   const int64_t batch = std::max<int64_t>(tblk, ((1ll << 27) / nsplit) / tblk * tblk);
   const int64_t Tb = std::min<int64_t>(T, batch);
   CUDA_TRY(c, part.ensure(sizeof(double) * std::max<int64_t>(Tb, 1) * nsplit));
   for (int64_t t0 = 0; t0 < T; t0 += batch) {
     const int64_t n = std::min<int64_t>(batch, T - t0);
     dim3 grid((unsigned)nblk(n, (int)tblk), (unsigned)nsplit);
-    if (zero_check)
-      k_far<true><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(n, txy + t0, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                            c->d_sq.as<double>(), chunk, part.as<double>(),
-                                                            0x3ff00000u);
-    else
-      k_far<false><<<grid, FAR_THREADS, kFarSmem, c->fs>>>(n, txy + t0, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
-                                                             c->d_sq.as<double>(), chunk, part.as<double>(),
-                                                             0x3ff00000u);
+    auto kern = zero_check ? (R == 4 ? k_far<true, 4> : k_far<true, FAR_R>) : (R == 4 ? k_far<false, 4> : k_far<false, FAR_R>);
+    kern<<<grid, FAR_THREADS, kFarSmem, c->fs>>>(n, txy + t0, S, c->d_sx.as<double>(), c->d_sy.as<double>(),
+                                                 c->d_sq.as<double>(), chunk, part.as<double>(), 0x3ff00000u);
     k_far_reduce<<<nblk(n, 256), 256, 0, c->fs>>>(n, nsplit, part.as<double>(), ufar + t0);
     c->far_launches += 2;
   }
@@ -3947,7 +3956,9 @@ int vp_create(int device, vp_ctx** out) {
   for (int n2 = 0; n2 <= kMaxPdev; ++n2)
     for (int m = 0; m <= n2; ++m) cn[koorn_index(m, n2)] = std::sqrt((double)((2 * m + 1) * (2 * n2 + 2)));
   if (cudaFuncSetAttribute(k_far<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_far<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess) {
+      cudaFuncSetAttribute(k_far<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_far<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_far<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFarSmem) != cudaSuccess) {
     vp_destroy(c);
     return 3;
   }
