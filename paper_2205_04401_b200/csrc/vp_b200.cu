@@ -452,9 +452,11 @@ __device__ __forceinline__ double warp_point_sum(int lane, int64_t e, int len_q,
 // ---------------------------------------------------------------------------
 // K4: near_eval in two stages.
 //  K4a k_near_leaves<FILL>: one thread per (target, element) pair runs the
-//      4-way midpoint subdivision depth-first (child 0 first: the oracle's
-//      recursion order) and counts / writes its accepted leaves as path
-//      codes (2 bits per level, depth in the top 6 bits).
+//      4-way midpoint subdivision depth-first and counts / writes its accepted
+//      leaves as path codes (2 bits per level, depth in the top 6 bits).  The
+//      leaf SET and every counter are the oracle's; the ORDER differs (the
+//      four children of a node are tested together and the accepted ones
+//      emitted at once), which only reorders the per-pair sums.
 //  K4b k_near_int<P>: one warp per pair integrates the pair's leaves with the
 //      N_n rule, lanes over (leaf, node) two nodes at a time, and subtracts
 //      the element's far-field point sum.
@@ -601,7 +603,7 @@ struct LeafOut {
 // per pair leaves most lanes of a warp idle behind its largest pair.  Each
 // warp instead owns a chunk of `chunk` pairs (kLeafChunk; 32 = one pair per
 // lane for the few overflow pairs of the fill pass); a lane walks one pair at a
-// time (its own DFS, so a pair's leaves keep the oracle's order), and lanes
+// time (its own DFS; leaf order as described for K4a), and lanes
 // whose pair is done take the chunk's next pair (ballot + prefix count: the
 // assignment is warp-synchronous, and a pair's outputs do not depend on it).
 constexpr int kLeafChunk = 128;
