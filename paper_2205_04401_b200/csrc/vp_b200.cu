@@ -34,6 +34,15 @@ namespace {
 
 constexpr int kMaxPdev = 12;
 constexpr int kMaxModes = (kMaxPdev + 1) * (kMaxPdev + 2) / 2;  // 91
+// K5 samples the density from monomial coefficients about the reference
+// centroid for p <= kMonoMaxP (27 DFMA per point at p = 6 instead of the
+// ~120-op Koornwinder recurrence); the monomial basis costs a factor
+// (|K| coefficient growth) 1e2 / 1e3 in rounding at p = 6 / 8 for rough
+// densities, none for smooth ones; above p = 8 the growth is
+// 1e5+, so K5 keeps the recurrence.
+constexpr int kMonoMaxP = 8;
+constexpr int kMonoMaxModes = (kMonoMaxP + 1) * (kMonoMaxP + 2) / 2;  // 45
+constexpr double kMonoC0 = 1.0 / 3.0;  // expansion centre (c0, c0), exactly this double
 constexpr int kMaxFar = 1024;
 constexpr int kMaxNearRule = 256;
 constexpr int kMaxGL = 64;
@@ -125,6 +134,30 @@ __global__ void k_sources(int64_t E, int len_q, int M, const ElemRec* __restrict
   double f = 0.0;
   for (int j = 0; j < M; ++j) f = fma(c[j], v[j], f);
   sq[s] = (R->far_w[i] * T.det) * f * kInv4Pi;
+}
+
+// Per-element monomial coefficients of the density about the reference
+// centroid c0 = (1/3, 1/3) (double-rounded), for the self kernel's density
+// samples: mono[e, i] = sum_j coeffs[e, j] Kmon[j, i], Kmon the exact
+// (long double) expansion of c_j K_j (upload_self_tab).  p <= kMonoMaxP only.
+__global__ void __launch_bounds__(256) k_mono(int64_t E, int M, const double* __restrict__ coeffs,
+                                              const double* __restrict__ kmon, double* __restrict__ mono) {
+  __shared__ double sk[kMonoMaxModes * kMonoMaxModes];
+  for (int i = threadIdx.x; i < M * M; i += blockDim.x) sk[i] = kmon[i];
+  __syncthreads();
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= E * M) return;
+  const int64_t e = o / M;
+  const int i = (int)(o - e * M);
+  const double* c = coeffs + e * M;
+  double s0 = 0.0, s1 = 0.0;
+  int j = 0;
+  for (; j + 2 <= M; j += 2) {
+    s0 = fma(c[j], sk[j * M + i], s0);
+    s1 = fma(c[j + 1], sk[(j + 1) * M + i], s1);
+  }
+  if (j < M) s0 = fma(c[j], sk[j * M + i], s0);
+  mono[o] = s0 + s1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1806,6 +1839,36 @@ struct SelfTab {
   double T2[2 * (kMaxPdev + 1) * kMaxModes];
 };
 
+// f at NPT points from its monomial coefficients about the reference centroid
+// (k_mono): (X, Y) = (xi, eta) - c0, coefficient of X^i Y^j at
+// mono_off(P, j) + i; Horner in X per power of Y, then in Y.  NPT points
+// share every coefficient load.
+__host__ __device__ constexpr int mono_off(int P, int j) { return j * (P + 1) - j * (j - 1) / 2; }
+template <int P, int NPT, class CC>
+__device__ __forceinline__ void density_mono(const CC& cc, const double* X, const double* Y, double* out) {
+  double f[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) f[q] = cc[mono_off(P, P)];
+#pragma unroll
+  for (int j = P - 1; j >= 0; --j) {
+    const int oj = mono_off(P, j);
+    double r[NPT];
+    const double top = cc[oj + P - j];
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) r[q] = top;
+#pragma unroll
+    for (int i = P - j - 1; i >= 0; --i) {
+      const double ci = cc[oj + i];
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) r[q] = fma(r[q], X[q], ci);
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) f[q] = fma(f[q], Y[q], r[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) out[q] = f[q];
+}
+
 // Per target the warp handles the three sub-triangles together where their
 // work is independent: lanes 0-2 form the three side geometries, the
 // density samples of all three (3 M points) share one pass of the warp, and
@@ -1815,30 +1878,52 @@ struct SelfSide {
   double Ax, Ay, ABx, ABy, L, h, st, avx, avy, BRx, BRy, invL;
   int N, Mr, npan, degenerate, pad;
 };
-template <int P>
+template <int GS>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One target per group of GS lanes (GS = 16: two targets per warp, so the
+// per-target phases whose width is below 32 -- the three side geometries,
+// the panel compaction, the moment contraction -- serve two targets per warp
+// instruction).  Every loop has a warp-uniform trip count (the maximum over
+// the warp's groups) and per-group predicates, so the warp never diverges
+// between groups and full-mask shuffles stay valid.
+#ifndef VP_SELF_GS
+#define VP_SELF_GS 16
+#endif
+template <int P, int GS>
 __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
            const double2* __restrict__ txy, const ElemRec* __restrict__ el,
            const double* __restrict__ coeffs, const double* __restrict__ sx,
            const double* __restrict__ sy, const double* __restrict__ sq, const RulesDev* __restrict__ R,
            const SelfTab* __restrict__ ST, double* __restrict__ corr, double* __restrict__ sub_out,
-           int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV) {
+           int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV,
+           const double* __restrict__ mono) {
+  static_assert(GS == 16 || GS == 32, "k_self: 16 or 32 lanes per target");
+  constexpr int NG = 32 / GS;             // targets per warp
+  constexpr int NGB = SELF_WARPS * NG;    // targets per block
   constexpr int M = (P + 1) * (P + 2) / 2;
   constexpr int NP = P + 1;
   constexpr int M3 = 3 * M;
+  constexpr bool kMono = P <= kMonoMaxP;  // density samples from mono (k_mono)
   // density samples per lane and pass over the 3 M points of a target
 #ifndef VP_SELF_SNPT_MAX
-#define VP_SELF_SNPT_MAX 5
+#define VP_SELF_SNPT_MAX 6
 #endif
-  constexpr int SNPT0 = M3 <= 32 ? 1 : (M3 <= 64 ? 2 : (M3 <= 96 ? 3 : (M3 <= 128 ? 4 : 5)));
-  constexpr int SNPT = SNPT0 < VP_SELF_SNPT_MAX ? SNPT0 : VP_SELF_SNPT_MAX;
-  __shared__ double scc[SELF_WARPS][M];
-  __shared__ double sF[SELF_WARPS][M3], sE[SELF_WARPS][3][2 * NP];
-  // non-empty panels of the side in progress: sl = a + b x_gl (panel middle and
-  // half width over L), weight h (half width) w_gl
-  __shared__ double sPa[SELF_WARPS][kMaxSelfPanels + 8], sPb[SELF_WARPS][kMaxSelfPanels + 8],
-      sPc[SELF_WARPS][kMaxSelfPanels + 8];
-  __shared__ SelfSide sS[SELF_WARPS][3];
+  // (the fewest passes with at most VP_SELF_SNPT_MAX points per lane, then
+  // the fewest points per lane for that many passes)
+  constexpr int SNPASS = (M3 + GS * VP_SELF_SNPT_MAX - 1) / (GS * VP_SELF_SNPT_MAX);
+  constexpr int SNPT = (M3 + GS * SNPASS - 1) / (GS * SNPASS);
+  // panels compacted per chunk (the node loop runs after each chunk); one
+  // zero-weight pad entry at index GS
+  __shared__ double scc[NGB][M];
+  __shared__ double sF[NGB][M3], sE[NGB][3][2 * NP];
+  __shared__ double sPa[NGB][GS + 1], sPb[NGB][GS + 1], sPc[NGB][GS + 1];
+  __shared__ SelfSide sS[NGB][3];
   constexpr bool kHorner = P <= kSelfHornerMaxP;
   extern __shared__ __align__(16) double sT2[];  // [2 NP][M], dynamic
   __shared__ double ssr[M], sss[M], sla[NP], slb[NP];
@@ -1859,32 +1944,45 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     sla[i] = ST->la[i];
     slb[i] = ST->lb[i];
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* cc = scc[wid];
-  double* F = sF[wid];
+  const int gl = lane & (GS - 1), grp = lane / GS;
+  const int g = wid * NG + grp;  // the group's slot in the block's shared arrays
+  if (gl == 0) {                 // pad panel: weight 0 at the side's middle
+    sPa[g][GS] = 0.5;
+    sPb[g][GS] = 0.0;
+    sPc[g][GS] = 0.0;
+  }
+  __syncthreads();
+  double* cc = scc[g];
+  double* F = sF[g];
   unsigned long long my_panels = 0, my_degen = 0;
-  for (int64_t it = (int64_t)blockIdx.x * SELF_WARPS + wid; it < n_items;
-       it += (int64_t)gridDim.x * SELF_WARPS) {
-    const int32_t t = item_tgt ? item_tgt[it] : (int32_t)it;
-    const int32_t e = item_elem[it];
-    if (e < 0) {
-      if (lane == 0) {
-        corr[it] = 0.0;
-        if (sub_out) sub_out[it] = 0.0;
-        if (panels_out) panels_out[it] = 0;
-      }
-      continue;
+  for (int64_t base = ((int64_t)blockIdx.x * SELF_WARPS + wid) * NG; base < n_items;
+       base += (int64_t)gridDim.x * NGB) {
+    const int64_t it = base + grp;
+    const bool have = it < n_items;
+    const int32_t t = !have ? 0 : (item_tgt ? item_tgt[it] : (int32_t)it);
+    const int32_t e_raw = have ? item_elem[it] : -1;
+    if (have && e_raw < 0 && gl == 0) {
+      corr[it] = 0.0;
+      if (sub_out) sub_out[it] = 0.0;
+      if (panels_out) panels_out[it] = 0;
     }
-    if (curve_id_of(CV, e) >= 0) continue;  // curved element: k_self_curved
-    const double2 tp = txy[t];
+    // an inactive group (no item, target outside, curved element: k_self_curved)
+    // runs along on element 0 with every side marked empty and writes nothing
+    const bool act = e_raw >= 0 && curve_id_of(CV, e_raw) < 0;
+    const int32_t e = act ? e_raw : 0;
+    const double2 tp = txy[act ? t : 0];
     const double tx = tp.x, ty = tp.y;
     const ElemRec& Er = el[e];
     __syncwarp();
-    for (int j = lane; j < M; j += 32) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
-    if (lane < 3) {
+    if constexpr (kMono) {
+      for (int j = gl; j < M; j += GS) cc[j] = mono[(int64_t)e * M + j];
+    } else {
+      for (int j = gl; j < M; j += GS) cc[j] = coeffs[(int64_t)e * M + j] * c_cn[j];
+    }
+    if (gl < 3) {
       // side (A, B) = (v_k, v_{k+1}); reference corners (0,0), (1,0), (0,1)
-      const int k = lane;
+      const int k = gl;
       double txi, teta;
       rn_locate(Er, tx, ty, txi, teta);
       const double Ax = k == 0 ? Er.x0 : (k == 1 ? Er.x1 : Er.x2);
@@ -1894,33 +1992,42 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
       SelfGeom G;
       self_geom(tx, ty, Ax, Ay, Bx, By, G);
       const double Arx = k == 1 ? 1.0 : 0.0, Ary = k == 2 ? 1.0 : 0.0;
-      SelfSide& S = sS[wid][k];
+      SelfSide& S = sS[g][k];
       S.Ax = G.Ax; S.Ay = G.Ay; S.ABx = G.ABx; S.ABy = G.ABy; S.L = G.L; S.h = G.h; S.st = G.st;
       S.invL = 1.0 / G.L;
       S.avx = Arx - txi;  // A - v in reference coordinates
       S.avy = Ary - teta;
       S.BRx = (k == 0 ? 1.0 : 0.0) - Arx;
       S.BRy = (k == 1 ? 1.0 : 0.0) - Ary;
-      S.N = G.N; S.Mr = G.Mr; S.npan = min(G.npan, kMaxSelfPanels); S.degenerate = G.degenerate ? 1 : 0;
+      S.N = G.N; S.Mr = G.Mr;
+      S.degenerate = G.degenerate ? 1 : 0;
+      // panels the node loop visits: none for a degenerate side or an inactive group
+      S.npan = (act && !G.degenerate) ? min(G.npan, kMaxSelfPanels) : 0;
     }
     double txi, teta;
     rn_locate(Er, tx, ty, txi, teta);
+    if constexpr (kMono) {  // displacements from the centroid of the monomial expansion
+      txi -= kMonoC0;
+      teta -= kMonoC0;
+    }
     __syncwarp();
     // (1) f at the M Fekete-type samples y = v + r (A - v) + s (B - A) of each
     // sub-triangle (f has total degree <= p in (r, s)); the 3 M points of the
-    // target in one pass, SNPT per lane (degenerate sides are computed and
-    // not used)
-    for (int i = SNPT * lane; i < M3; i += 32 * SNPT) {
+    // target, SNPT per lane and pass (degenerate sides are computed and not used)
+    for (int i = SNPT * gl; i < M3; i += GS * SNPT) {
       double xs[SNPT], ys[SNPT], f[SNPT];
 #pragma unroll
       for (int q = 0; q < SNPT; ++q) {
         const int iq = min(i + q, M3 - 1);
         const int k = iq >= 2 * M ? 2 : (iq >= M ? 1 : 0), sq_ = iq - k * M;
-        const SelfSide& S = sS[wid][k];
+        const SelfSide& S = sS[g][k];
         xs[q] = fma(sss[sq_], S.BRx, fma(ssr[sq_], S.avx, txi));
         ys[q] = fma(sss[sq_], S.BRy, fma(ssr[sq_], S.avy, teta));
       }
-      density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
+      if constexpr (kMono)
+        density_mono<P, SNPT>(ShCoef(cc), xs, ys, f);
+      else
+        density_n<P, SNPT>(ShCoef(cc), xs, ys, f);
 #pragma unroll
       for (int q = 0; q < SNPT; ++q)
         if (i + q < M3) F[i + q] = f[q];
@@ -1929,12 +2036,11 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     // (2) the sigma polynomials of the GGQ-rule moments per side, (Eb, Ec) =
     // T2 f (Gauss-Legendre grid interpolation, Legendre transforms in r and
     // sigma and the moment contraction, folded on the host)
-    for (int o = lane; o < 3 * 2 * NP; o += 32) {
+    for (int o = gl; o < 3 * 2 * NP; o += GS) {
       const int k = o >= 4 * NP ? 2 : (o >= 2 * NP ? 1 : 0), oo = o - k * 2 * NP;
       const double* Fk = F + k * M;
       const double* Tk = sT2 + oo * M;
-      // four independent DFMA chains: one chain of M dependent DFMAs was the
-      // kernel's top stall (ncu source page)
+      // four independent DFMA chains
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int q = 0;
 #pragma unroll 2
@@ -1945,54 +2051,26 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         s3 = fma(Tk[q + 3], Fk[q + 3], s3);
       }
       for (; q < M; ++q) s0 = fma(Tk[q], Fk[q], s0);
-      sE[wid][k][oo] = (s0 + s1) + (s2 + s3);
+      sE[g][k][oo] = (s0 + s1) + (s2 + s3);
     }
     __syncwarp();
     double acc = 0.0;
     long long npan_item = 0;
+    if (act && gl == 0)
+      my_degen += (unsigned long long)(sS[g][0].degenerate + sS[g][1].degenerate + sS[g][2].degenerate);
 #pragma unroll 1
     for (int k = 0; k < 3; ++k) {
-      const SelfSide& S = sS[wid][k];
-      if (S.degenerate) {
-        ++my_degen;  // identical in every lane; counted once below
-        continue;
-      }
+      const SelfSide& S = sS[g][k];
       SelfGeom G;
       G.Ax = S.Ax; G.Ay = S.Ay; G.ABx = S.ABx; G.ABy = S.ABy; G.L = S.L; G.h = S.h; G.st = S.st;
       G.N = S.N; G.Mr = S.Mr;
-      const double* Eb = sE[wid][k];
+      const double* Eb = sE[g][k];
       const double* Ec = Eb + NP;
-      // (3) arc-length nodes: dyadic panels x Gauss-Legendre.
-      // The side's non-empty panels are compacted once (ballot) into (a, b, c)
-      // with sl = s / L = a + b x_gl and node weight c w_gl = (half width) h w_gl,
-      // so the node loop has no empty-panel test; the side's sigma polynomials
-      // (Eb pre-halved: log r0 = log(r0^2) / 2) sit in registers.
       const int npan = S.npan;
+      int npan_w = npan;  // warp-uniform chunk loop bound
+#pragma unroll
+      for (int o = 16; o >= GS; o >>= 1) npan_w = max(npan_w, __shfl_xor_sync(0xffffffffu, npan_w, o));
       const double invL = S.invL;
-      int nne = 0;
-      for (int i0 = 0; i0 < npan; i0 += 32) {
-        const int i = i0 + lane;
-        const double s0 = i <= npan ? self_bnd(G, i) : 0.0;
-        double s1 = __shfl_down_sync(0xffffffffu, s0, 1);
-        if (lane == 31) s1 = i + 1 <= npan ? self_bnd(G, i + 1) : 0.0;
-        const bool ne = i < npan && s1 > s0;
-        const unsigned bal = __ballot_sync(0xffffffffu, ne);
-        if (ne) {
-          const int pos = nne + __popc(bal & ((1u << lane) - 1u));
-          const double half = 0.5 * (s1 - s0);
-          sPa[wid][pos] = (0.5 * (s0 + s1)) * invL;
-          sPb[wid][pos] = half * invL;
-          sPc[wid][pos] = half * G.h;
-        }
-        nne += __popc(bal);
-      }
-      npan_item += nne;
-      if (lane < 8) {  // zero-weight pad panels: the grouped node loop needs no bound test
-        sPa[wid][nne + lane] = 0.0;
-        sPb[wid][nne + lane] = 0.0;
-        sPc[wid][nne + lane] = 0.0;
-      }
-      __syncwarp();
       double eb[NP], ec[NP];
 #pragma unroll
       for (int kk = 0; kk < NP; ++kk) {
@@ -2000,8 +2078,9 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         ec[kk] = Ec[kk];
       }
       const double dAx = G.Ax - tx, dAy = G.Ay - ty;
-      auto node = [&](int pp, double xg, double wg) {
-        const double sl = fma(sPb[wid][pp], xg, sPa[wid][pp]);
+      auto node = [&](int pp, bool ok, double xg, double wg) {
+        const int pc = ok ? pp : GS;  // the pad entry for an idle slot
+        const double sl = fma(sPb[g][pc], xg, sPa[g][pc]);
         const double ddx = fma(sl, G.ABx, dAx), ddy = fma(sl, G.ABy, dAy);
         const double lg = fast_log_r2<1>(sltab, fma(ddx, ddx, ddy * ddy));
         const double x = fma(2.0, sl, -1.0);
@@ -2031,33 +2110,68 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
             q1 = q2;
           }
         }
-        acc = fma(sPc[wid][pp] * wg, fma(lg, ib, ic), acc);
+        const double v = fma(sPc[g][pc] * wg, fma(lg, ib, ic), acc);
+        acc = ok ? v : acc;
       };
-      if (NL == 16) {  // the default N_l: lane l keeps node l mod 16; two independent
-                       // nodes per lane and pass (panels pp, pp + 2; pads weigh 0)
-        const double xg = sglx[lane & 15], wg = sglw[lane & 15];
+      // (3) arc-length nodes: dyadic panels x Gauss-Legendre,
+      // in chunks of GS panels: the chunk's non-empty panels are compacted
+      // (ballot) into (a, b, c) with sl = s / L = a + b x_gl and node weight
+      // c w_gl = (half width) h w_gl
+#pragma unroll 1
+      for (int i0 = 0; i0 < npan_w; i0 += GS) {
+        const int i = i0 + gl;
+        const double s0 = i <= npan ? self_bnd(G, i) : 0.0;
+        double s1 = __shfl_down_sync(0xffffffffu, s0, 1, GS);
+        if (gl == GS - 1) s1 = i + 1 <= npan ? self_bnd(G, i + 1) : 0.0;
+        const bool ne = i < npan && s1 > s0;
+        const unsigned bal = (__ballot_sync(0xffffffffu, ne) >> (grp * GS)) & (GS == 32 ? 0xffffffffu : 0xffffu);
+        if (ne) {
+          const int pos = __popc(bal & ((1u << gl) - 1u));
+          const double half = 0.5 * (s1 - s0);
+          sPa[g][pos] = (0.5 * (s0 + s1)) * invL;
+          sPb[g][pos] = half * invL;
+          sPc[g][pos] = half * G.h;
+        }
+        const int nne = __popc(bal);
+        npan_item += nne;
+        int nne_w = nne;
+#pragma unroll
+        for (int o = 16; o >= GS; o >>= 1) nne_w = max(nne_w, __shfl_xor_sync(0xffffffffu, nne_w, o));
+        __syncwarp();
+        if (NL == 16) {  // the default N_l: lane l keeps node l mod 16
+          const double xg = sglx[gl & 15], wg = sglw[gl & 15];
 #ifndef VP_SELF_NODES
 #define VP_SELF_NODES 2
 #endif
-        for (int pp = lane >> 4; pp < nne; pp += 2 * VP_SELF_NODES) {
+          constexpr int PS = GS / 16;  // panels side by side in a group
+          for (int pp = gl >> 4; pp < nne_w; pp += PS * VP_SELF_NODES) {
 #pragma unroll
-          for (int u = 0; u < VP_SELF_NODES; ++u) node(pp + 2 * u, xg, wg);
+            for (int u = 0; u < VP_SELF_NODES; ++u) node(pp + PS * u, pp + PS * u < nne, xg, wg);
+          }
+        } else {
+          const int nodes_w = nne_w * NL;
+          int pi = gl / NL, gq = gl - pi * NL;
+          for (int j = gl; j < nodes_w; j += GS, gq += GS) {
+            while (gq >= NL) { gq -= NL; ++pi; }
+            node(pi, pi < nne, sglx[gq], sglw[gq]);
+          }
         }
-      } else {
-        const int nodes = nne * NL;
-        int pi = lane / NL, gq = lane - pi * NL;
-        for (int j = lane; j < nodes; j += 32, gq += 32) {
-          while (gq >= NL) { gq -= NL; ++pi; }
-          node(pi, sglx[gq], sglw[gq]);
-        }
+        __syncwarp();
       }
-      __syncwarp();
     }
-    const double val = warp_sum(acc) * kInv2Pi;
+    const double val = group_sum<GS>(acc) * kInv2Pi;
     // the evaluation subtracts every point sum of t at once (k_psum_tgt); the
     // per-pair API returns this element's own
-    const double sub = sub_out ? warp_point_sum(lane, e, len_q, tx, ty, sx, sy, sq, sltab, true) : 0.0;
-    if (lane == 0) {
+    double sub = 0.0;
+    if (sub_out) {
+      for (int i = gl; i < len_q; i += GS) {
+        const int64_t kq = (int64_t)e * len_q + i;
+        const double dx = tx - sx[kq], dy = ty - sy[kq];
+        sub = fma(sq[kq], fast_log_r2<1, true>(sltab, fma(dx, dx, dy * dy)), sub);
+      }
+      sub = group_sum<GS>(sub);
+    }
+    if (act && gl == 0) {
       corr[it] = val;
       if (sub_out) sub_out[it] = sub;
       if (panels_out) panels_out[it] = npan_item;
@@ -2065,12 +2179,8 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     }
     __syncwarp();
   }
-  if (lane == 0) {
-    if (my_panels) atomicAdd(&stats[3], my_panels);
-  } else {
-    my_degen = 0;
-  }
-  if (lane == 0 && my_degen) atomicAdd(&stats[4], my_degen);
+  if (gl == 0 && my_panels) atomicAdd(&stats[3], my_panels);
+  if (gl == 0 && my_degen) atomicAdd(&stats[4], my_degen);
 }
 inline size_t self_dyn_smem(int p) { return sizeof(double) * 2 * (p + 1) * koorn_size(p); }
 
@@ -2575,6 +2685,7 @@ struct vp_ctx {
   // density
   int p = -1, M = 0;
   DevBuf d_coeffs, d_V;
+  DevBuf d_kmon, d_mono;  // p <= kMonoMaxP: basis -> centroid monomials [M x M]; per-element monomials [E x M]
   // sources
   DevBuf d_sx, d_sy, d_sq;
   // per-evaluation scratch
@@ -3144,11 +3255,11 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
 template <int P>
 void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
                  double* corr, double* sub, int64_t* panels) {
-  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS), (int64_t)c->sm_count * 64);
-  k_self<P><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->ss>>>(
+  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS * (32 / VP_SELF_GS)), (int64_t)c->sm_count * 64);
+  k_self<P, VP_SELF_GS><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->ss>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
       c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
-      sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c));
+      sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c), c->d_mono.as<double>());
   if (has_curves(c)) {
     const int cb = (int)std::min<int64_t>(nblk(n, CURV_WARPS), (int64_t)c->sm_count * 16);
     k_self_curved<P><<<std::max(cb, 1), CURV_WARPS * 32, 0, c->ss>>>(
@@ -3390,6 +3501,73 @@ int self_sample_map(vp_ctx* c, SelfTab& T, const double* gx_m11) {
   return 0;
 }
 
+// Kmon [M x M]: row j = the monomial coefficients of c_j K_j (the normalised
+// Koornwinder basis of koorn.cuh / koornwinder.hpp:12-21) in (X, Y) =
+// (xi - c0, eta - c0), c0 = kMonoC0, column mono_off(p, j') + i' for
+// X^i' Y^j'.  Built by the basis recurrences of koorn_eval carried out on
+// bivariate polynomials in long double, so each entry is the exact
+// coefficient up to long-double rounding.
+static void mono_table(int p, std::vector<double>& out) {
+  const int n = p + 1, M = koorn_size(p);
+  using Poly = std::vector<long double>;  // [i * n + j] = coefficient of X^i Y^j, i + j <= p
+  auto zero = [&] { return Poly((size_t)n * n, 0.0L); };
+  auto mul = [&](const Poly& a, const Poly& b) {
+    Poly r = zero();
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; i + j < n; ++j) {
+        const long double av = a[(size_t)i * n + j];
+        if (av == 0.0L) continue;
+        for (int k = 0; i + k < n; ++k)
+          for (int l = 0; i + j + k + l < n; ++l) r[(size_t)(i + k) * n + j + l] += av * b[(size_t)k * n + l];
+      }
+    return r;
+  };
+  auto lin = [&](long double a, const Poly& x, long double b, const Poly& y) {
+    Poly r = zero();
+    for (size_t i = 0; i < r.size(); ++i) r[i] = a * x[i] + b * y[i];
+    return r;
+  };
+  const long double c0 = (long double)kMonoC0;
+  Poly one = zero(), x = zero(), y = zero();
+  one[0] = 1.0L;
+  x[0] = c0;
+  y[0] = c0;
+  if (p >= 1) {
+    x[(size_t)1 * n] = 1.0L;
+    y[1] = 1.0L;
+  }
+  const Poly v = lin(1.0L, one, -1.0L, x);  // 1 - x
+  const Poly u = lin(2.0L, y, -1.0L, v);    // 2y - (1 - x)
+  const Poly v2 = mul(v, v);
+  const Poly t = lin(2.0L, x, -1.0L, one);  // 2x - 1
+  std::vector<Poly> L{one};
+  if (p >= 1) L.push_back(u);
+  for (int m = 1; m + 1 <= p; ++m)
+    L.push_back(lin((long double)(2 * m + 1) / (m + 1), mul(u, L[m]), -(long double)m / (m + 1), mul(v2, L[m - 1])));
+  out.assign((size_t)M * M, 0.0);
+  for (int m = 0; m <= p; ++m) {
+    const long double a = 2 * m + 1;
+    std::vector<Poly> P{one};
+    if (m + 1 <= p) P.push_back(lin(0.5L * (a + 2.0L), t, 0.5L * a, one));
+    for (int k = 1; m + k + 1 <= p; ++k) {
+      const long double kk = k;
+      const long double c1 = 2 * (kk + 1) * (kk + a + 1) * (2 * kk + a);
+      const long double c2 = (2 * kk + a + 1) * (a * a);
+      const long double c3 = (2 * kk + a) * (2 * kk + a + 1) * (2 * kk + a + 2);
+      const long double c4 = 2 * (kk + a) * kk * (2 * kk + a + 2);
+      Poly nx = lin(c2 / c1, P[k], c3 / c1, mul(t, P[k]));
+      P.push_back(lin(1.0L, nx, -c4 / c1, P[k - 1]));
+    }
+    for (int k = 0; m + k <= p; ++k) {
+      const int nn = m + k, row = koorn_index(m, nn);
+      const long double cn = std::sqrt((long double)((2 * m + 1) * (2 * nn + 2)));
+      const Poly b = mul(P[k], L[m]);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; i + j < n; ++j) out[(size_t)row * M + mono_off(p, j) + i] = (double)(cn * b[(size_t)i * n + j]);
+    }
+  }
+}
+
 // SelfTab for the current (p, GGQ rule): Gauss-Legendre interpolation grid
 // on [0,1], Legendre projection weights and the GGQ-rule moments.
 int upload_self_tab(vp_ctx* c) {
@@ -3446,6 +3624,12 @@ int upload_self_tab(vp_ctx* c) {
       }
   }
   if (int rc = self_sample_map(c, T, gx)) return rc;
+  if (c->p <= kMonoMaxP) {
+    std::vector<double> km;
+    mono_table(c->p, km);
+    CUDA_TRY(c, c->d_kmon.ensure(sizeof(double) * km.size()));
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_kmon.p, km.data(), sizeof(double) * km.size(), cudaMemcpyHostToDevice, c->stream));
+  }
   CUDA_TRY(c, c->d_selftab.ensure(sizeof(SelfTab)));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_selftab.p, &T, sizeof(SelfTab), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -3473,6 +3657,13 @@ int compute_sources(vp_ctx* c) {
                                                   c->d_coeffs.as<double>(), c->d_V.as<double>(),
                                                   c->d_rules.as<RulesDev>(), c->d_sx.as<double>(),
                                                   c->d_sy.as<double>(), c->d_sq.as<double>());
+  if (c->p <= kMonoMaxP) {  // K5's density samples
+    const int64_t n = c->n_tri * c->M;
+    CUDA_TRY(c, c->d_mono.ensure(sizeof(double) * n));
+    k_mono<<<nblk(n, 256), 256, 0, c->stream>>>(c->n_tri, c->M, c->d_coeffs.as<double>(), c->d_kmon.as<double>(),
+                                                c->d_mono.as<double>());
+    c->last_launches += 1;
+  }
   if (has_curves(c)) {
     const int64_t nc = (int64_t)c->h_celist.size();
     k_sources_curved<<<nblk(nc * c->rules.len_q, 128), 128, 0, c->stream>>>(
@@ -3986,19 +4177,19 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_near_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cg<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cache_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)near_cache_mma_smem(kMaxModes)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(0)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(1)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(2)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(3)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(4)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(5)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(6)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(7)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(8)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(9)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<0, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(0)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<1, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(1)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<2, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(2)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<3, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(3)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<4, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(4)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<5, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(5)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<6, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(6)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<7, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(7)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<8, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(8)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<9, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(9)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<10, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<11, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<12, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
