@@ -162,7 +162,10 @@ __global__ void __launch_bounds__(256) k_mono(int64_t E, int M, const double* __
 
 // ---------------------------------------------------------------------------
 // element binning for the list build: every element is entered in each grid
-// cell its near-field bbox overlaps.
+// cell its near-field bbox overlaps.  Cell size in units of the median
+// near-field extent B: a target scans ~ (1 + cs / B)^2 bboxes' worth of
+// elements, the bins hold ~ (1 + B / cs)^2 entries per element.
+constexpr double kGridScale = 0.25;
 __device__ __forceinline__ int cell_coord(double x, double x0, double inv_cs, int n) {
   const double f = floor(rn_mul(rn_sub(x, x0), inv_cs));
   int c = f < 0.0 ? 0 : (f >= (double)n ? n - 1 : (int)f);
@@ -1049,6 +1052,121 @@ inline size_t near_cache_mma_smem(int M) {
   return sizeof(double) * ((size_t)kNcBM * nc_stride(Kp) + (size_t)Kp * nc_stride(kNcBN));
 }
 
+// The same GEMM with the tile of V held in shared memory: a block keeps
+// V[:, r0 .. r0 + 128) (all M modes of 128 cache rows) and walks kNc2EB
+// consecutive 32-element blocks, so V is staged once per 32 tiles instead of
+// once per tile and the only per-tile staging is the 32 x M coefficients,
+// prefetched one element block ahead with cp.async (two buffers).  A warp owns
+// 32 of the 128 rows: 4 x 4 DMMA m8n8k4 tiles, the same k order and the same
+// coeffs * det products as k_near_cache_mma, so the cache is bit-identical.
+// Row block fastest in the grid: the 33 row blocks of an element chunk run
+// together and share its coefficients in L2.
+constexpr int kNc2BN = 128, kNc2EB = 32;
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__global__ void __launch_bounds__(128)
+    k_near_cache_mma2(int64_t E, int M, int64_t R, const double* __restrict__ Vt, const double* __restrict__ coeffs,
+                      const ElemRec* __restrict__ el, double* __restrict__ out, const uint8_t* __restrict__ used) {
+  extern __shared__ __align__(16) double ncs[];
+  const int Kp = (M + 3) & ~3;
+  const int SA = nc_stride(Kp), SB = nc_stride(kNc2BN);
+  double* Bs = ncs;                      // [Kp][SB]
+  double* As0 = ncs + (size_t)Kp * SB;   // two buffers [kNcBM][SA]
+  __shared__ double sdet[2][kNcBM];
+  const int64_t nrb = (R + kNc2BN - 1) / kNc2BN;
+  const int64_t r0 = ((int64_t)blockIdx.x % nrb) * kNc2BN;
+  const int64_t nblk_e = (E + kNcBM - 1) / kNcBM;
+  const int64_t b0 = ((int64_t)blockIdx.x / nrb) * kNc2EB, b1 = min(b0 + kNc2EB, nblk_e);
+  for (int i = threadIdx.x; i < Kp * kNc2BN; i += blockDim.x) {
+    const int j = i / kNc2BN, n = i - j * kNc2BN;
+    const int64_t r = r0 + n;
+    Bs[j * SB + n] = (j < M && r < R) ? __ldg(Vt + (int64_t)j * R + r) : 0.0;
+  }
+  for (int i = threadIdx.x; i < 2 * kNcBM * SA; i += blockDim.x) As0[i] = 0.0;  // k padding stays zero
+  __syncthreads();
+  // stage element block b into buffer s: coefficients by cp.async, det by a plain store
+  auto stage = [&](int64_t b, int s) {
+    double* As = As0 + (size_t)s * kNcBM * SA;
+    const int64_t e0 = b * kNcBM;
+    const int rows = (int)min((int64_t)kNcBM, E - e0);
+    const double* src = coeffs + e0 * M;
+    for (int i = threadIdx.x; i < kNcBM * M; i += blockDim.x) {
+      const int m = i / M, j = i - m * M;
+      if (m < rows) cp_async8(As + m * SA + j, src + i);
+      else As[m * SA + j] = 0.0;
+    }
+    if (threadIdx.x < kNcBM) sdet[s][threadIdx.x] = threadIdx.x < rows ? el[e0 + threadIdx.x].det : 0.0;
+    asm volatile("cp.async.commit_group;");
+  };
+  auto wanted = [&](int64_t b) {  // block-uniform: some element of the block is in the call's pairs
+    if (!used) return true;
+    const int64_t e0 = b * kNcBM;
+    bool any = false;
+    for (int m = 0; m < kNcBM && e0 + m < E; ++m) any |= used[e0 + m] != 0;
+    return any;
+  };
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  int64_t b = b0;
+  while (b < b1 && !wanted(b)) ++b;
+  if (b < b1) stage(b, 0);
+  int s = 0;
+  while (b < b1) {
+    int64_t bn = b + 1;
+    while (bn < b1 && !wanted(bn)) ++bn;
+    if (bn < b1) {
+      stage(bn, s ^ 1);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
+    }
+    __syncthreads();
+    const double* As = As0 + (size_t)s * kNcBM * SA;
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    double dt[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) dt[mi] = sdet[s][mi * 8 + g];
+    for (int k0 = 0; k0 < Kp; k0 += 4) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = As[(mi * 8 + g) * SA + k0 + t] * dt[mi];  // |J_T| folded in
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bb[ni] = Bs[(k0 + t) * SB + w * 32 + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[mi][ni][0]), "+d"(acc[mi][ni][1])
+              : "d"(a[mi]), "d"(bb[ni]));
+    }
+    const int64_t e0 = b * kNcBM;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int64_t e = e0 + mi * 8 + g;
+      if (e >= E) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int64_t r = r0 + w * 32 + ni * 8 + 2 * t;
+        if (r < R) out[e * R + r] = acc[mi][ni][0];
+        if (r + 1 < R) out[e * R + r + 1] = acc[mi][ni][1];
+      }
+    }
+    __syncthreads();  // the buffer is free for the stage after next
+    b = bn;
+    s ^= 1;
+  }
+}
+inline size_t near_cache_mma2_smem(int M) {
+  const int Kp = (M + 3) & ~3;
+  return sizeof(double) * (2 * (size_t)kNcBM * nc_stride(Kp) + (size_t)Kp * nc_stride(kNc2BN));
+}
+
 // NPT leaf nodes per call share the density coefficient loads
 template <int P, int NPT>
 __device__ __forceinline__ double near_nodes(const ShCoef& cc, const double2* __restrict__ ltab,
@@ -1629,7 +1747,9 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
             // no branch for the last slot's missing nodes (49 = 6 x 8 + 1):
             // there nu = nv = 0 and g = 0, the log of |D0|^2 is finite (also
             // for zero rows: the bit-level log maps 0 to a finite value), so
-            // the slot adds exactly 0 and the warp does not diverge
+            // the slot adds exactly 0 and the warp does not diverge.  (Two
+            // register sets for g used alternately instead of the copy ran
+            // slower: 63.1 vs 55.7 ms on config 4.)
             const double dx = fma(-nu[k], ba.x, fma(-nv[k], ca.x, d0.x));
             const double dy = fma(-nu[k], ba.y, fma(-nv[k], ca.y, d0.y));
             double& a = (k & 1) ? acc1 : acc;  // two chains: K8 DFMAs deep -> K8 / 2
@@ -1696,7 +1816,7 @@ __global__ void __launch_bounds__(PT_WARPS * 32)
     k_psum_tgt(int64_t T, const double2* __restrict__ txy, const int32_t* __restrict__ self,
                const int64_t* __restrict__ off, const int32_t* __restrict__ ids, int len_q,
                const double* __restrict__ sx, const double* __restrict__ sy, const double* __restrict__ sq,
-               double* __restrict__ psum) {
+               double* __restrict__ psum, int idx32) {
   extern __shared__ __align__(16) double2 ptab[];
   for (int i = threadIdx.x; i < kLogEntries * COPIES; i += blockDim.x) ptab[i] = g_logtab[i / COPIES];
   __syncthreads();
@@ -1707,6 +1827,7 @@ __global__ void __launch_bounds__(PT_WARPS * 32)
   // comes from lane b of a per-target register list (one coalesced load) and
   // b = j / len_q from a multiply-high (exact for j < 32 * 600, len_q < 600).
   const unsigned magic = (unsigned)((1ull << 32) / (unsigned)len_q + 1ull);
+  const unsigned ulen = (unsigned)len_q;
   for (int64_t t = (int64_t)blockIdx.x * PT_WARPS + wid; t < T; t += (int64_t)gridDim.x * PT_WARPS) {
     const double2 tp = txy[t];
     const int32_t se = self[t];
@@ -1714,28 +1835,43 @@ __global__ void __launch_bounds__(PT_WARPS * 32)
     const int hs = se >= 0 ? 1 : 0;
     const int64_t nb = nn + hs;
     double s = 0.0, s1 = 0.0;
-    if (nb <= 32 && len_q < 600) {
+    if (nb <= 32 && len_q < 600 && idx32) {
       const int32_t my_e = lane < nb ? (lane < hs ? se : ids[o0 + lane - hs]) : 0;
-      const int items = (int)nb * len_q;
-      for (int j0 = 0; j0 < items; j0 += 128) {
-        double xs[4], ys[4], qs[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + lane + 32 * u;
-          const int jj = j < items ? j : 0;
-          const int bb = (int)__umulhi((unsigned)jj, magic);
-          const int32_t e = __shfl_sync(0xffffffffu, my_e, bb);
-          const int64_t k = (int64_t)e * len_q + (jj - bb * len_q);
-          xs[u] = sx[k];
-          ys[u] = sy[k];
-          qs[u] = j < items ? sq[k] : 0.0;
-        }
+      const unsigned items = (unsigned)nb * ulen, full = items & ~127u;
+      // source index of item j = b len_q + i: k = e_b len_q + i = j + (e_b - b) len_q,
+      // 32-bit (idx32: the mesh has fewer than 2^32 sources)
+      auto load = [&](unsigned j, double& x, double& y, double& q) {
+        const unsigned bb = __umulhi(j, magic);
+        const unsigned e = (unsigned)__shfl_sync(0xffffffffu, my_e, (int)bb);
+        const unsigned k = (e - bb) * ulen + j;
+        x = sx[k];
+        y = sy[k];
+        q = sq[k];
+      };
+      auto add = [&](const double* xs, const double* ys, const double* qs) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const double dx = tp.x - xs[u], dy = tp.y - ys[u];
           double& a = (u & 1) ? s1 : s;
           a = fma(qs[u], fast_log_r2<COPIES, false>(sltab, fma(dx, dx, dy * dy)), a);
         }
+      };
+      unsigned j0 = 0;
+      for (; j0 < full; j0 += 128) {  // whole passes: no bounds test
+        double xs[4], ys[4], qs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load(j0 + lane + 32 * u, xs[u], ys[u], qs[u]);
+        add(xs, ys, qs);
+      }
+      if (j0 < items) {  // the last, partial pass: idle slots re-read item 0 with q = 0
+        double xs[4], ys[4], qs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned j = j0 + lane + 32 * u;
+          load(j < items ? j : 0u, xs[u], ys[u], qs[u]);
+          qs[u] = j < items ? qs[u] : 0.0;
+        }
+        add(xs, ys, qs);
       }
     } else {  // long lists (all-near elements): element by element
       for (int64_t b = 0; b < nb; ++b) {
@@ -1769,6 +1905,27 @@ struct SelfGeom {
   bool degenerate;
 };
 
+// The oracle's panel count: the number of halvings n = 0, 1, .. (capped at
+// 1100) until x 2^-n < dmin (oracle self_eval's `for (x = st; !(x < dmin); x *= 0.5)`).
+// Halving is exact while x stays normal, so for normal positive x >= dmin the
+// count follows from the two exponents and one mantissa comparison: with
+// n0 = exponent(x) - exponent(dmin), x 2^-n0 has dmin's exponent and is below
+// dmin iff its mantissa is; one more halving always is.  Anything else
+// (zero, subnormal, non-finite) takes the loop itself.
+__device__ __forceinline__ int self_halvings(double x, double dmin) {
+  const long long bx = __double_as_longlong(x), bd = __double_as_longlong(dmin);
+  const int ex = (int)((bx >> 52) & 0x7ff), ed = (int)((bd >> 52) & 0x7ff);
+  if (bx > 0 && bd > 0 && ex > 0 && ed > 0 && ex < 0x7ff && ed < 0x7ff) {
+    if (x < dmin) return 0;
+    const long long mant = (1ll << 52) - 1;
+    const int n0 = ex - ed;
+    return min(n0 + ((bx & mant) < (bd & mant) ? 0 : 1), 1100);
+  }
+  int n = 0;
+  for (double y = x; !(y < dmin) && n < 1100; y *= 0.5) ++n;
+  return n;
+}
+
 __device__ __forceinline__ void self_geom(double tx, double ty, double Ax, double Ay, double Bx,
                                           double By, SelfGeom& G) {
   G.Ax = Ax;
@@ -1785,10 +1942,7 @@ __device__ __forceinline__ void self_geom(double tx, double ty, double Ax, doubl
   const double sl = rn_div(G.st, G.L);
   const double gx = rn_add(Ax, rn_mul(sl, G.ABx)), gy = rn_add(Ay, rn_mul(sl, G.ABy));
   const double dmin = rn_dist(tx, ty, gx, gy);
-  int N = 0;
-  for (double x = G.st; !(x < dmin) && N < 1100; x *= 0.5) ++N;
-  int Mr = 0;
-  for (double x = rn_sub(G.L, G.st); !(x < dmin) && Mr < 1100; x *= 0.5) ++Mr;
+  const int N = self_halvings(G.st, dmin), Mr = self_halvings(rn_sub(G.L, G.st), dmin);
   G.N = N;
   G.Mr = Mr;
   G.npan = N + Mr + 2;
@@ -1894,6 +2048,9 @@ __device__ __forceinline__ double group_sum(double v) {
 #ifndef VP_SELF_GS
 #define VP_SELF_GS 16
 #endif
+// lanes per target by order: 8-lane groups keep their per-group arrays within
+// the 48 KB of static shared memory up to p = 8
+constexpr int self_gs(int p) { return (VP_SELF_GS == 8 && p > 8) ? 16 : VP_SELF_GS; }
 template <int P, int GS>
 __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
     k_self(int64_t n_items, const int32_t* __restrict__ item_tgt, const int32_t* __restrict__ item_elem,
@@ -1903,7 +2060,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
            const SelfTab* __restrict__ ST, double* __restrict__ corr, double* __restrict__ sub_out,
            int64_t* __restrict__ panels_out, unsigned long long* __restrict__ stats, CurvesDev CV,
            const double* __restrict__ mono) {
-  static_assert(GS == 16 || GS == 32, "k_self: 16 or 32 lanes per target");
+  static_assert(GS == 8 || GS == 16 || GS == 32, "k_self: 8, 16 or 32 lanes per target");
   constexpr int NG = 32 / GS;             // targets per warp
   constexpr int NGB = SELF_WARPS * NG;    // targets per block
   constexpr int M = (P + 1) * (P + 2) / 2;
@@ -2124,7 +2281,7 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
         double s1 = __shfl_down_sync(0xffffffffu, s0, 1, GS);
         if (gl == GS - 1) s1 = i + 1 <= npan ? self_bnd(G, i + 1) : 0.0;
         const bool ne = i < npan && s1 > s0;
-        const unsigned bal = (__ballot_sync(0xffffffffu, ne) >> (grp * GS)) & (GS == 32 ? 0xffffffffu : 0xffffu);
+        const unsigned bal = (__ballot_sync(0xffffffffu, ne) >> (grp * GS)) & (GS == 32 ? 0xffffffffu : ((1u << (GS & 31)) - 1u));
         if (ne) {
           const int pos = __popc(bal & ((1u << gl) - 1u));
           const double half = 0.5 * (s1 - s0);
@@ -2138,12 +2295,18 @@ __global__ void __launch_bounds__(SELF_WARPS * 32, VP_SELF_MINB)
 #pragma unroll
         for (int o = 16; o >= GS; o >>= 1) nne_w = max(nne_w, __shfl_xor_sync(0xffffffffu, nne_w, o));
         __syncwarp();
-        if (NL == 16) {  // the default N_l: lane l keeps node l mod 16
+        if (GS == 8 && NL == 16) {  // lane l keeps nodes l and l + 8 of every panel
+          const double xg0 = sglx[gl & 7], wg0 = sglw[gl & 7], xg1 = sglx[(gl & 7) + 8], wg1 = sglw[(gl & 7) + 8];
+          for (int pp = 0; pp < nne_w; ++pp) {
+            node(pp, pp < nne, xg0, wg0);
+            node(pp, pp < nne, xg1, wg1);
+          }
+        } else if (NL == 16) {  // the default N_l: lane l keeps node l mod 16
           const double xg = sglx[gl & 15], wg = sglw[gl & 15];
 #ifndef VP_SELF_NODES
 #define VP_SELF_NODES 2
 #endif
-          constexpr int PS = GS / 16;  // panels side by side in a group
+          constexpr int PS = GS >= 16 ? GS / 16 : 1;  // panels side by side in a group
           for (int pp = gl >> 4; pp < nne_w; pp += PS * VP_SELF_NODES) {
 #pragma unroll
             for (int u = 0; u < VP_SELF_NODES; ++u) node(pp + PS * u, pp + PS * u < nne, xg, wg);
@@ -2944,6 +3107,11 @@ int build_elements(vp_ctx* c) {
     double cs = ext[ext.size() / 2];
     const double W = gx1 - gx0, H = gy1 - gy0;
     if (!(cs > 0.0)) cs = std::max(W, H);
+    cs *= kGridScale;
+    if (const char* gs = getenv("VP_GRID_SCALE")) {  // A/B switch: cell size in median extents
+      const double f = atof(gs);
+      if (f > 0.0) cs *= f / kGridScale;
+    }
     while ((W / cs + 1) * (H / cs + 1) > double(1 << 24)) cs *= 1.5;
     G.x0 = gx0;
     G.y0 = gy0;
@@ -3255,8 +3423,8 @@ int launch_near(vp_ctx* c, int64_t n, const int32_t* ptgt, const int32_t* pelem,
 template <int P>
 void launch_self(vp_ctx* c, int64_t n, const int32_t* itgt, const int32_t* ielem, const double2* txy,
                  double* corr, double* sub, int64_t* panels) {
-  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS * (32 / VP_SELF_GS)), (int64_t)c->sm_count * 64);
-  k_self<P, VP_SELF_GS><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->ss>>>(
+  const int blocks = (int)std::min<int64_t>(nblk(n, SELF_WARPS * (32 / self_gs(P))), (int64_t)c->sm_count * 64);
+  k_self<P, self_gs(P)><<<std::max(blocks, 1), SELF_WARPS * 32, self_dyn_smem(P), c->ss>>>(
       n, itgt, ielem, txy, c->d_el.as<ElemRec>(), c->d_coeffs.as<double>(), c->d_sx.as<double>(),
       c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_rules.as<RulesDev>(), c->d_selftab.as<SelfTab>(), corr,
       sub, panels, c->d_stats.as<unsigned long long>(), curves_dev(c), c->d_mono.as<double>());
@@ -3365,7 +3533,15 @@ int build_near_cache(vp_ctx* c, const int32_t* pelem, int64_t n_pairs) {
   CUDA_TRY(c, c->d_gcache.ensure(sizeof(double) * (size_t)(c->n_tri * R + Ln + 64)));
   CUDA_TRY(c, cudaMemsetAsync(c->d_gcache.as<double>() + c->n_tri * R, 0, sizeof(double) * (Ln + 64), c->stream));
   static const bool cache_simt = getenv("VP_NEAR_CACHE_SIMT") != nullptr;  // A/B switch: DFMA kernel
-  if (!cache_simt) {
+  static const bool cache_mma1 = getenv("VP_NEAR_CACHE_MMA1") != nullptr;  // A/B switch: one tile per block
+  if (!cache_simt && !cache_mma1) {
+    const int64_t nchunk = ((c->n_tri + kNcBM - 1) / kNcBM + kNc2EB - 1) / kNc2EB;
+    const int64_t nb = nchunk * nblk(R, kNc2BN);
+    if (nb > (int64_t)INT32_MAX) return set_err(c, 1, "near cache: too many blocks");
+    k_near_cache_mma2<<<(unsigned)nb, 128, near_cache_mma2_smem(M), c->stream>>>(
+        c->n_tri, M, R, c->d_cacheV.as<double>(), c->d_coeffs.as<double>(), c->d_el.as<ElemRec>(),
+        c->d_gcache.as<double>(), used);
+  } else if (!cache_simt) {
     const int64_t nb = (int64_t)((c->n_tri + kNcBM - 1) / kNcBM) * nblk(R, kNcBN);
     if (nb > (int64_t)INT32_MAX) return set_err(c, 1, "near cache: too many blocks");
     k_near_cache_mma<<<(unsigned)nb, 128, near_cache_mma_smem(M), c->stream>>>(
@@ -4008,7 +4184,8 @@ int evaluate_impl(vp_ctx* c, int64_t T, const double2* txy, double* u, vp_stats*
     auto psum_args = [&](auto kern, int copies) {
       kern<<<pblocks, PT_WARPS * 32, sizeof(double2) * kLogEntries * copies, c->s3>>>(
           T, txy, c->d_self.as<int32_t>(), c->d_off.as<int64_t>(), c->d_ids.as<int32_t>(), c->rules.len_q,
-          c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_psum.as<double>());
+          c->d_sx.as<double>(), c->d_sy.as<double>(), c->d_sq.as<double>(), c->d_psum.as<double>(),
+          (int64_t)c->n_tri * c->rules.len_q < (1ll << 32) ? 1 : 0);
     };
     switch (c->psum_copies) {
       case 2: psum_args(k_psum_tgt<2>, 2); break;
@@ -4177,19 +4354,20 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_near_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cg<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_cache_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)near_cache_mma_smem(kMaxModes)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<0, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(0)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<1, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(1)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<2, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(2)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<3, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(3)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<4, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(4)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<5, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(5)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<6, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(6)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<7, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(7)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<8, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(8)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<9, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(9)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<10, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<11, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_self<12, VP_SELF_GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_cache_mma2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)near_cache_mma2_smem(kMaxModes)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<0, self_gs(0)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(0)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<1, self_gs(1)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(1)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<2, self_gs(2)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(2)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<3, self_gs(3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(3)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<4, self_gs(4)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(4)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<5, self_gs(5)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(5)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<6, self_gs(6)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(6)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<7, self_gs(7)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(7)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<8, self_gs(8)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(8)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<9, self_gs(9)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(9)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<10, self_gs(10)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<11, self_gs(11)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_self<12, self_gs(12)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
