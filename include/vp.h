@@ -176,6 +176,16 @@ int vp_self_pairs(vp_ctx* ctx, int64_t n_pairs, const double* txy, const int32_t
  * (the subtract-and-add split of SPEC.md:612-615). */
 int vp_set_far_method(vp_ctx* ctx, int method, int order, int leaf_size);
 
+/* The FMM order from a far-field tolerance (fmm_eval's eps_fmm):
+ * vp_fmm_order_for returns the smallest supported order whose far-field error
+ * against the direct sum (relative max-norm, calibrated on the BASELINE
+ * configurations) is below eps_fmm: 7, 11, .., 31; below 1e-13 the order
+ * stays 31 (error floor 8e-15).  vp_set_fmm_tolerance = vp_set_far_method(ctx,
+ * 1, vp_fmm_order_for(eps_fmm), leaf_size); eps_fmm outside (0, 1) is a usage
+ * error. */
+int vp_fmm_order_for(double eps_fmm);
+int vp_set_fmm_tolerance(vp_ctx* ctx, double eps_fmm, int leaf_size);
+
 /* Potential interpolation.  interp_coeffs (rules.hpp:
  * 165-170): per-element Koornwinder coefficients [n_elem * M_p] from values
  * at the M_p reference nodes (ref_x, ref_y) of an interpolation rule, e.g.

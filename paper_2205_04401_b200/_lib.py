@@ -94,6 +94,8 @@ _SIGS = [
     ("vp_set_near_model", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
     ("vp_set_near_cache", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
     ("vp_set_far_method", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("vp_fmm_order_for", ctypes.c_int, [ctypes.c_double]),
+    ("vp_set_fmm_tolerance", ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int]),
     ("vp_device_info", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("vp_shard_bounds", ctypes.c_int, [ctypes.c_int64, c_int64_p, ctypes.c_int, c_int64_p]),

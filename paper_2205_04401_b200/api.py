@@ -512,6 +512,11 @@ class Evaluator:
         m = {"direct": 0, "fmm": 1, "none": 2}[method]
         _check(self._L.vp_set_far_method(self._h, m, order, leaf_size), self._err())
 
+    def set_fmm_tolerance(self, eps_fmm: float, leaf_size: int = 0):
+        """FMM far field with the order chosen from eps_fmm (fmm_eval's
+        tolerance); see fmm_order_for."""
+        _check(self._L.vp_set_fmm_tolerance(self._h, float(eps_fmm), leaf_size), self._err())
+
     def set_near_model(self, model: str = "precise", ball_factor: float = 1.5):
         """'precise' (Bernstein ellipses, default) or 'ball' (SPEC.md:585 baseline)."""
         m = {"precise": 0, "ball": 1}[model]
@@ -692,11 +697,21 @@ def evaluate_field(pr: Problem, targets=None, device: int = 0):
     return u, st
 
 
-def fmm_eval(pr: Problem, targets=None, direct: bool = False, order: int = 0, device: int = 0):
+def fmm_order_for(eps_fmm: float) -> int:
+    """The expansion order the library uses for a far-field tolerance eps_fmm."""
+    return int(_lib.lib().vp_fmm_order_for(float(eps_fmm)))
+
+
+def fmm_eval(pr: Problem, targets=None, direct: bool = False, order: int = 0, device: int = 0,
+             eps_fmm: float = 0.0):
     """fmm_eval: far field of all quadrature-node charges at
-    the targets, by the GPU FMM or, with direct=True, the O(N^2) path."""
+    the targets, by the GPU FMM (order from eps_fmm when given)
+    or, with direct=True, the O(N^2) path."""
     with Evaluator(device) as ev:
         ev.load(pr)
         if not direct:
-            ev.set_far_method("fmm", order)
+            if eps_fmm > 0.0:
+                ev.set_fmm_tolerance(eps_fmm)
+            else:
+                ev.set_far_method("fmm", order)
         return ev.far_field(pr.txy if targets is None else targets)

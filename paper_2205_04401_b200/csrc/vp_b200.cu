@@ -2903,6 +2903,7 @@ struct vp_ctx {
   int tabs_p = -1;  // p of the density-independent tables (K1's V, near-cache Vt, SelfTab); -1: stale
   int cacheV_depth = -2, cacheV_p = -1;
   DevBuf f_tk, f_tk2, f_tv, f_tord;  // FMM: target leaf keys and the leaf order of the targets
+  DevBuf f_active;                  // FMM: boxes holding targets (the downward pass skips the others)
   DevBuf f_tab, f_keys, f_keys2, f_vals, f_idx, f_beg, f_end, f_pxy, f_pq, f_mp, f_lp, f_flag, f_oidx,
       f_otxy, f_ou, f_cnt;
   // far field on its own stream and host thread when it overlaps the near and
@@ -3961,6 +3962,25 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   k_fmm_gather<<<nblk(S, 256), 256, 0, c->fs>>>(S, c->f_idx.as<int32_t>(), c->d_sx.as<double>(),
                                                      c->d_sy.as<double>(), c->d_sq.as<double>(),
                                                      c->f_pxy.as<double2>(), c->f_pq.as<double>());
+  // targets in leaf order (stable radix sort by leaf key) and the boxes that hold them
+  CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tk.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tk2.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tv.ensure(sizeof(int32_t) * (T + 1)));
+  CUDA_TRY(c, c->f_tord.ensure(sizeof(int32_t) * (T + 1)));
+  k_fmm_tkeys<<<nblk(T, 256), 256, 0, c->fs>>>(T, txy, g, c->f_tk.as<int32_t>(), c->f_tv.as<int32_t>());
+  tmpb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(), c->f_tv.as<int32_t>(),
+                                  c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
+  CUDA_TRY(c, c->f_tmp.ensure(tmpb));
+  cub::DeviceRadixSort::SortPairs(c->f_tmp.p, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(),
+                                  c->f_tv.as<int32_t>(), c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
+  CUDA_TRY(c, c->f_active.ensure((size_t)nbox));
+  static const bool all_boxes = getenv("VP_FMM_ALL_BOXES") != nullptr;  // A/B switch: no skipping
+  CUDA_TRY(c, cudaMemsetAsync(c->f_active.p, all_boxes ? 1 : 0, (size_t)nbox, c->fs));
+  k_fmm_mark_leaves<<<nblk(T, 256), 256, 0, c->fs>>>(T, c->f_tk.as<int32_t>(), L, c->f_active.as<uint8_t>());
+  for (int l = L - 1; l >= 2; --l)
+    k_fmm_mark_parents<<<nblk(1ll << (2 * l), 256), 256, 0, c->fs>>>(l, c->f_active.as<uint8_t>());
   // upward pass
   const int wblocks = (int)std::min<int64_t>(nblk(nleaf, kFmmThreads / 32), (int64_t)c->sm_count * 64);
   const size_t sm_p2m = sizeof(double2) * (kFmmThreads / 32) * 32 * (size_t)(P1 | 1);
@@ -3979,26 +3999,20 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
   for (int l = 2; l <= L; ++l) {
     const int64_t nb = 1ll << (2 * l);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblk(nb, kFmmThreads / 32), (int64_t)c->sm_count * 64));
-    if (P1 == 32)
-      k_fmm_m2l32<<<blocks, kFmmThreads, 0, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
-                                                          c->f_lp.as<double2>());
-    else
-      k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
-                                                            c->f_lp.as<double2>());
+#define VP_M2L_CASE(N)                                                                                   \
+  case N:                                                                                                \
+    k_fmm_m2l32<N><<<blocks, kFmmThreads, 0, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(), \
+                                                      c->f_lp.as<double2>(), c->f_active.as<uint8_t>()); \
+    break;
+    switch (P1) {  // one coefficient per lane for the orders of vp_fmm_order_for
+      VP_M2L_CASE(8) VP_M2L_CASE(12) VP_M2L_CASE(16) VP_M2L_CASE(20) VP_M2L_CASE(24) VP_M2L_CASE(28) VP_M2L_CASE(32)
+      default:
+        k_fmm_m2l<<<blocks, kFmmThreads, sm_m2l, c->fs>>>(g, l, c->f_tab.as<double>(), c->f_mp.as<double2>(),
+                                                          c->f_lp.as<double2>(), c->f_active.as<uint8_t>());
+    }
+#undef VP_M2L_CASE
   }
-  // L2P + P2P over the targets in leaf order (stable radix sort by leaf key)
-  CUDA_TRY(c, c->f_flag.ensure(sizeof(int32_t) * (T + 1)));
-  CUDA_TRY(c, c->f_tk.ensure(sizeof(int32_t) * (T + 1)));
-  CUDA_TRY(c, c->f_tk2.ensure(sizeof(int32_t) * (T + 1)));
-  CUDA_TRY(c, c->f_tv.ensure(sizeof(int32_t) * (T + 1)));
-  CUDA_TRY(c, c->f_tord.ensure(sizeof(int32_t) * (T + 1)));
-  k_fmm_tkeys<<<nblk(T, 256), 256, 0, c->fs>>>(T, txy, g, c->f_tk.as<int32_t>(), c->f_tv.as<int32_t>());
-  tmpb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(), c->f_tv.as<int32_t>(),
-                                  c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
-  CUDA_TRY(c, c->f_tmp.ensure(tmpb));
-  cub::DeviceRadixSort::SortPairs(c->f_tmp.p, tmpb, c->f_tk.as<int32_t>(), c->f_tk2.as<int32_t>(),
-                                  c->f_tv.as<int32_t>(), c->f_tord.as<int32_t>(), (int)T, 0, 2 * L + 1, c->fs);
+  // L2P + P2P over the targets in leaf order
   const size_t sm_eval = sizeof(LogTab);
   if (zero_check)
     k_fmm_eval<true><<<nblk(T, 256), 256, sm_eval, c->fs>>>(
@@ -4010,7 +4024,7 @@ int fmm_far_sum(vp_ctx* c, int64_t T, const double2* txy, double* ufar, bool zer
         c->f_lp.as<double2>(), ufar, c->f_flag.as<int32_t>(), 0x3ff00000u, c->f_tord.as<int32_t>());
   c->far_launches += 3;
   CUDA_TRY(c, cudaGetLastError());
-  c->far_launches += 7 + 2 * (L - 1);
+  c->far_launches += 8 + 3 * (L - 1) - 1;
   // targets outside the root box: direct far sum
   CUDA_TRY(c, c->f_oidx.ensure(sizeof(int32_t) * (T + 1)));
   CUDA_TRY(c, c->f_cnt.ensure(sizeof(int64_t)));
@@ -4462,6 +4476,27 @@ int vp_set_far_method(vp_ctx* c, int method, int order, int leaf_size) {
   c->fmm_p = order ? order : 31;  // p + 1 = 32 coefficients: one per lane
   c->fmm_leaf = leaf_size ? leaf_size : 40;
   return 0;
+}
+
+// eps_fmm -> expansion order.  The far-field error of the FMM
+// against the direct sum, relative max-norm, measured on configs 1-4 by order
+// (profiles/r02_fmm_order_sweep.json, tools/fmm_tolerance.py), stays below
+// 0.15 * 0.41^p down to the rounding floor of 8e-15 at p = 31; the order is
+// the smallest p with that bound <= eps_fmm, rounded up so that p + 1 is a
+// multiple of four in [8, 32] (the orders k_fmm_m2l32 is instantiated for).
+int vp_fmm_order_for(double eps_fmm) {
+  if (!(eps_fmm > 0.0)) return 31;
+  const double p = std::ceil(std::log(eps_fmm / 0.15) / std::log(0.41));
+  int P1 = 4 * (int)std::ceil((std::max(p, 0.0) + 1.0) / 4.0);
+  P1 = std::max(8, std::min(32, P1));
+  return P1 - 1;
+}
+
+int vp_set_fmm_tolerance(vp_ctx* c, double eps_fmm, int leaf_size) {
+  if (!c) return 1;
+  if (!(eps_fmm > 0.0) || !(eps_fmm < 1.0))
+    return set_err(c, 1, "set_fmm_tolerance: eps_fmm must be in (0, 1)");
+  return vp_set_far_method(c, 1, vp_fmm_order_for(eps_fmm), leaf_size);
 }
 
 int vp_device_info(vp_ctx* c, int* sm_count, int* cc_major, int* cc_minor) {

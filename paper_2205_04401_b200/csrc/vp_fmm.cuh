@@ -152,6 +152,28 @@ __global__ void k_fmm_tkeys(int64_t T, const double2* __restrict__ txy, FmmGeom 
   vals[t] = (int32_t)t;
 }
 
+// Boxes whose local expansion the evaluation needs: the leaves that hold a
+// target and their ancestors.  The downward pass (M2L + L2L) skips the rest,
+// so a shard of the targets pays for its own part of the tree only; with
+// targets in every leaf nothing is skipped.  A box's expansion does not
+// depend on which other boxes are computed: u(t) stays bitwise the same.
+__global__ void k_fmm_mark_leaves(int64_t T, const int32_t* __restrict__ keys, int L, uint8_t* __restrict__ active) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int64_t nleaf = 1ll << (2 * L);
+  const int32_t k = keys[t];
+  if ((int64_t)k < nleaf) active[lvl_off(L) + k] = 1;
+}
+__global__ void k_fmm_mark_parents(int l, uint8_t* __restrict__ active) {
+  const int n = 1 << l;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= (int64_t)n * n) return;
+  const int ix = (int)(b % n), iy = (int)(b / n);
+  const uint8_t* ch = active + lvl_off(l + 1);
+  const int64_t c0 = (int64_t)(2 * iy) * (2 * n) + 2 * ix;
+  active[lvl_off(l) + b] = ch[c0] | ch[c0 + 1] | ch[c0 + 2 * n] | ch[c0 + 2 * n + 1];
+}
+
 __global__ void k_fmm_gather(int64_t S, const int32_t* __restrict__ idx, const double* __restrict__ sx,
                              const double* __restrict__ sy, const double* __restrict__ sq,
                              double2* __restrict__ pxy, double* __restrict__ pq) {
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(kFmmThreads)
 // One warp per box; lanes own coefficients l = lane, lane + 32.
 __global__ void __launch_bounds__(kFmmThreads)
     k_fmm_m2l(FmmGeom g, int l, const double* __restrict__ tab, const double2* __restrict__ mp,
-              double2* __restrict__ lp) {
+              double2* __restrict__ lp, const uint8_t* __restrict__ active) {
   extern __shared__ double fsh[];
   FmmTabLayout TL(g.p);
   const int P1 = TL.P1;
@@ -305,6 +327,7 @@ __global__ void __launch_bounds__(kFmmThreads)
   const double logh = log(h);
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbox;
        b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (!active[lvl_off(l) + b]) continue;  // no target below this box
     const int ix = (int)(b % n), iy = (int)(b / n);
     double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
     if (l >= 3) {  // L2L from the parent (levels 0-2 carry no local expansion)
@@ -375,14 +398,16 @@ __global__ void __launch_bounds__(kFmmThreads)
   }
 }
 
-// The same downward pass specialised to p = 31 (32 coefficients, one per
-// lane): lane l keeps its column binA[1..31][l] of the M2L binomial matrix in
-// registers, so each source box costs 31 broadcast loads of e_k and 62 DFMA
-// per lane instead of two shared loads per pair of DFMA.
+// The same downward pass specialised to P1 = p + 1 <= 32 coefficients, one per
+// lane: lane l keeps its column binA[1..p][l] of the M2L binomial matrix in
+// registers, so each source box costs p broadcast loads of e_k and 2 p DFMA
+// per lane instead of two shared loads per pair of DFMA.  Instantiated for
+// the orders vp_fmm_order_for returns (P1 = 8, 12, .., 32; lanes >= P1 idle).
+template <int P1>
 __global__ void __launch_bounds__(kFmmThreads)
     k_fmm_m2l32(FmmGeom g, int l, const double* __restrict__ tab, const double2* __restrict__ mp,
-                double2* __restrict__ lp) {
-  constexpr int P1 = 32;
+                double2* __restrict__ lp, const uint8_t* __restrict__ active) {
+  static_assert(P1 >= 2 && P1 <= 32, "one coefficient per lane");
   __shared__ double binB[P1 * P1];
   __shared__ double2 dpow[4 * P1];
   __shared__ double2 ebuf[kFmmThreads / 32][P1];
@@ -393,7 +418,7 @@ __global__ void __launch_bounds__(kFmmThreads)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double bc[P1];
 #pragma unroll
-  for (int k = 1; k < P1; ++k) bc[k] = tab[TL.binA + k * P1 + lane];
+  for (int k = 1; k < P1; ++k) bc[k] = lane < P1 ? tab[TL.binA + k * P1 + lane] : 0.0;
   __syncthreads();
   double2* e = ebuf[wid];
   const double inv_l = lane > 0 ? 1.0 / lane : 0.0;
@@ -404,6 +429,7 @@ __global__ void __launch_bounds__(kFmmThreads)
   const double logh = log(h);
   for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nbox;
        b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (!active[lvl_off(l) + b]) continue;  // no target below this box
     const int ix = (int)(b % n), iy = (int)(b / n);
     double2 acc = make_double2(0.0, 0.0);
     if (l >= 3) {  // L2L from the parent (levels 0-2 carry no local expansion)
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(kFmmThreads)
       const double2* par = lp + (lvl_off(l - 1) + (int64_t)py * (n >> 1) + px) * P1;
       const double2* dp = dpow + c * P1;
       __syncwarp();
-      e[lane] = par[lane];
+      if (lane < P1) e[lane] = par[lane];
       __syncwarp();
       double2 s = make_double2(0.0, 0.0);
       for (int k = lane; k < P1; ++k) {
@@ -429,7 +455,7 @@ __global__ void __launch_bounds__(kFmmThreads)
         const int dxi = cx - ix, dyi = cy - iy;
         if (dxi >= -1 && dxi <= 1 && dyi >= -1 && dyi <= 1) continue;
         const double2* src = mp + (lvl_off(l) + (int64_t)cy * n + cx) * P1;
-        const double2 a = src[lane];
+        const double2 a = lane < P1 ? src[lane] : make_double2(0.0, 0.0);
         const double Q = __shfl_sync(0xffffffffu, a.x, 0);
         const int o = (dyi + 3) * 7 + (dxi + 3);
         const double* mpw = tab + TL.mpow + (size_t)o * P1 * 2;
@@ -438,7 +464,8 @@ __global__ void __launch_bounds__(kFmmThreads)
         const bool any = Q != 0.0 || (lane >= 1 && (a.x != 0.0 || a.y != 0.0));
         if (!__any_sync(0xffffffffu, any)) continue;  // empty source box
         __syncwarp();
-        e[lane] = lane == 0 ? make_double2(0.0, 0.0) : cmul(a, make_double2(mpw[2 * lane], mpw[2 * lane + 1]));
+        if (lane < P1)
+          e[lane] = lane == 0 ? make_double2(0.0, 0.0) : cmul(a, make_double2(mpw[2 * lane], mpw[2 * lane + 1]));
         __syncwarp();
         double2 s = make_double2(0.0, 0.0);
 #pragma unroll
@@ -446,13 +473,13 @@ __global__ void __launch_bounds__(kFmmThreads)
         if (lane == 0) {
           acc.x += s.x + Q * (logh + tab[TL.logd + o]);
           acc.y += s.y;
-        } else {
+        } else if (lane < P1) {
           s.x -= Q * inv_l;
           acc = cfma(s, make_double2(dnv[2 * lane], dnv[2 * lane + 1]), acc);
         }
       }
     }
-    lp[(lvl_off(l) + b) * P1 + lane] = acc;
+    if (lane < P1) lp[(lvl_off(l) + b) * P1 + lane] = acc;
   }
 }
 

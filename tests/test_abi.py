@@ -144,3 +144,13 @@ def test_cpp_caller_builds_and_refuses_without_device():
         pytest.skip("a GPU is present (run by tests/test_gpu_r02.py)")
     r = subprocess.run([exe, "/tmp/vp_abi_caller_u.bin"], capture_output=True, text=True)
     assert r.returncode == 3, (r.returncode, r.stderr)
+
+
+def test_fmm_order_for_tolerance():
+    """eps_fmm -> order: monotone, p + 1 a multiple of four in
+    [8, 32], the default order at the evaluation tolerance."""
+    orders = [vp.fmm_order_for(e) for e in (1e-1, 1e-2, 1e-4, 1e-6, 1e-8, 1e-10, 1e-12, 1e-14, 1e-30)]
+    assert orders == sorted(orders)
+    assert all((p + 1) % 4 == 0 and 7 <= p <= 31 for p in orders)
+    assert orders[0] == 7 and vp.fmm_order_for(1e-8) == 19 and vp.fmm_order_for(1e-12) == 31 and orders[-1] == 31
+    assert vp.fmm_order_for(0.0) == 31 and vp.fmm_order_for(float("nan")) == 31
