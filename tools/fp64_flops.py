@@ -26,7 +26,7 @@ MET = {"gpu__time_duration.sum": "ns",
        "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul",
        "sm__ops_path_tensor_src_fp64.sum": "dmma"}  # DMMA flops (2 per FMA)
 # kernels of the near field (K4) and self (K5) stages of an evaluation
-NEAR_STAGE = ("k_near_leaves", "k_leaves_copy", "k_near_cache", "k_near_cache_mma", "k_near_c8", "k_near_cg", "k_near_ct", "k_near_int",
+NEAR_STAGE = ("k_near_leaves", "k_leaves_copy", "k_near_cache", "k_near_cache_mma", "k_near_cache_mma2", "k_near_c8", "k_near_cg", "k_near_ct", "k_near_int",
               "k_psum_tgt", "k_self", "k_near_combine", "k_pair_tgt")
 
 
