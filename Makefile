@@ -20,7 +20,7 @@ $(CSRC)/vp_b200.o: $(CSRC)/vp_b200.cu $(CSRC)/vp_device.cuh $(CSRC)/vp_curve.cuh
 		$(CSRC)/koorn.cuh include/vp.h include/vp_setup.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; exit 1)
 
-$(CSRC)/vp_setup.o: $(CSRC)/vp_setup.cpp $(CSRC)/koorn.cuh include/vp_setup.h
+$(CSRC)/vp_setup.o: $(CSRC)/vp_setup.cpp $(CSRC)/koorn.cuh $(CSRC)/sym_rules.inc include/vp_setup.h
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(CSRC)/vp_curves.o: $(CSRC)/vp_curves.cpp include/vp_setup.h

@@ -37,6 +37,13 @@ int vps_gauss_jacobi10(int n, double* x, double* w);
  * n = floor(order/2)+1 points per direction, len = n*n.  Query the length
  * with x == NULL. */
 int vps_simplex_rule(int order, int* len, double* x, double* y, double* w);
+/* The evaluation's far / near rule of order `order` (load_far_rule, rules.hpp:
+ * 121-125): a fully symmetric rule with positive weights and interior points,
+ * exact to degree `order`, computed by this repository's own moment-fitting
+ * solver (tools/make_sym_rules.py; degrees 6, 10 and 12: 12, 25 and 33
+ * points), else vps_simplex_rule's collapsed Gauss-Jacobi rule.  Same calling
+ * convention (x == NULL: only *len). */
+int vps_quad_rule(int order, int* len, double* x, double* y, double* w);
 
 /* Radial generalized Gaussian rule: ng+1 nodes on (0,1) integrating
  * r P_n(2r-1) and r log r P_n(2r-1), n <= ng (ggq.hpp:13-22, :96-182). */

@@ -100,6 +100,7 @@ def lib():
             "vpo_lattice_nodes": (i32, [i32, _d_p, _d_p]),
             "vpo_gauss_jacobi10": (i32, [i32, _d_p, _d_p]),
             "vpo_simplex_rule": (i32, [i32, ctypes.POINTER(i32), _d_p, _d_p, _d_p]),
+            "vpo_quad_rule": (i32, [i32, ctypes.POINTER(i32), _d_p, _d_p, _d_p]),
             "vpo_ggq": (i32, [i32, _d_p, _d_p, ctypes.POINTER(dbl)]),
             "vpo_density_eval": (dbl, [i32, _d_p, i32, dbl, dbl]),
             "vpo_project_density": (i32, [i64, _d_p, i64, _i32_p, i32, i32, _d_p, i32, _d_p]),
@@ -351,6 +352,15 @@ def simplex_rule(order):
     return x, y, w
 
 
+def quad_rule(order):
+    """The evaluation's far / near rule (symmetric where tabulated, else simplex_rule)."""
+    n = ctypes.c_int()
+    _check_in(lib().vpo_quad_rule(order, ctypes.byref(n), None, None, None))
+    x, y, w = (np.zeros(n.value) for _ in range(3))
+    _check_in(lib().vpo_quad_rule(order, ctypes.byref(n), _d(x), _d(y), _d(w)))
+    return x, y, w
+
+
 def gauss_jacobi10(n):
     x, w = np.zeros(n), np.zeros(n)
     _check_in(lib().vpo_gauss_jacobi10(n, _d(x), _d(w)))
@@ -386,8 +396,8 @@ class OracleRules:
 
     def __init__(self, q, n_n=12, n_l=16, n_g=8, eps=1e-12):
         self.q, self.n_n, self.n_g, self.eps = q, n_n, n_g, eps
-        self.far = simplex_rule(q)
-        self.near = simplex_rule(n_n)
+        self.far = quad_rule(q)
+        self.near = quad_rule(n_n)
         self.gl = gauss_legendre(n_l)
         r, w, _ = ggq(n_g)
         self.ggq = (r, w)

@@ -126,6 +126,7 @@ typedef struct {
 int vpo_lattice_nodes(int p, double* x, double* y);
 int vpo_gauss_jacobi10(int n, double* x, double* w);
 int vpo_simplex_rule(int order, int* len, double* x, double* y, double* w);
+int vpo_quad_rule(int order, int* len, double* x, double* y, double* w);
 int vpo_ggq(int ng, double* r, double* w, double* max_residual);
 double vpo_density_eval(int kind, const double* params, int n_params, double x, double y);
 int vpo_project_density(int64_t n_vert, const double* vxy, int64_t n_tri, const int32_t* tri, int p,

@@ -643,6 +643,57 @@ int vpo_simplex_rule(int order, int* len, double* x, double* y, double* w) {
   return 0;
 }
 
+// The evaluation's far / near rule (load_far_rule, rules.hpp:121-125): the
+// fully symmetric rule of that degree from the oracle's own copy of the
+// moment-fitted orbit table (tools/make_sym_rules.py), expanded orbit by
+// orbit; the collapsed Gauss-Jacobi rule for every other order.
+namespace {
+struct SymOrbits {
+  int degree, n1, n21, n111, points;
+  double p[64];
+};
+const SymOrbits kSymOrbits[] = {
+#include "sym_rules.inc"
+};
+}  // namespace
+
+int vpo_quad_rule(int order, int* len, double* x, double* y, double* w) {
+  const SymOrbits* r = nullptr;
+  for (const SymOrbits& t : kSymOrbits)
+    if (t.degree == order) r = &t;
+  if (!r) return vpo_simplex_rule(order, len, x, y, w);
+  if (!len) return in_fail(1, "quad_rule: len is null");
+  *len = r->points;
+  if (!x) return 0;
+  if (!y || !w) return in_fail(1, "quad_rule: null output array");
+  int n = 0;
+  const double* q = r->p;
+  if (r->n1) {
+    x[n] = 1.0 / 3.0;
+    y[n] = 1.0 / 3.0;
+    w[n++] = *q++;
+  }
+  for (int i = 0; i < r->n21; ++i, q += 2) {  // (a, a, c), c = 1 - 2a: (x, y) = (l2, l3)
+    const double a = q[1], c = 1.0 - 2.0 * a;
+    const double pts[3][2] = {{a, a}, {a, c}, {c, a}};
+    for (const auto& pt : pts) {
+      x[n] = pt[0];
+      y[n] = pt[1];
+      w[n++] = q[0];
+    }
+  }
+  for (int i = 0; i < r->n111; ++i, q += 3) {  // the six permutations of (a, b, c)
+    const double a = q[1], b = q[2], c = 1.0 - a - b;
+    const double pts[6][2] = {{a, b}, {b, a}, {a, c}, {c, a}, {b, c}, {c, b}};
+    for (const auto& pt : pts) {
+      x[n] = pt[0];
+      y[n] = pt[1];
+      w[n++] = q[0];
+    }
+  }
+  return 0;
+}
+
 int vpo_ggq(int ng, double* r, double* w, double* max_residual) {
   if (ng < 0 || ng > 20 || !r || !w) return in_fail(1, "ggq: order must be in [0, 20]");
   if (!Ggq(ng).solve(r, w, max_residual)) return in_fail(2, "ggq: moment fitting failed to converge");

@@ -111,6 +111,8 @@ _SIGS = [
     ("vps_gauss_jacobi10", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p]),
     ("vps_simplex_rule", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_double_p,
                                         c_double_p, c_double_p]),
+    ("vps_quad_rule", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_double_p,
+                                     c_double_p, c_double_p]),
     ("vps_ggq", ctypes.c_int, [ctypes.c_int, c_double_p, c_double_p, c_double_p]),
     ("vps_circle_arc", ctypes.c_int, [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_int, c_double_p, c_double_p, c_double_p]),

@@ -113,6 +113,18 @@ def simplex_rule(order: int):
     return x, y, w
 
 
+def quad_rule(order: int):
+    """(x, y, w) of the evaluation's far / near rule of order `order`
+    (load_far_rule, rules.hpp:121-125): the repository's own fully symmetric
+    rule where one is tabulated (degrees 6, 10, 12), else simplex_rule."""
+    L = _lib.lib()
+    n = ctypes.c_int()
+    _check(L.vps_quad_rule(order, ctypes.byref(n), None, None, None), _setup_err())
+    x, y, w = (np.zeros(n.value) for _ in range(3))
+    _check(L.vps_quad_rule(order, ctypes.byref(n), _d(x), _d(y), _d(w)), _setup_err())
+    return x, y, w
+
+
 def gauss_legendre(n: int):
     """Gauss-Legendre on [-1, 1] (gauss.hpp:17-46)."""
     x, w = np.zeros(n), np.zeros(n)
@@ -159,7 +171,7 @@ class Rules:
 
 def make_rules(q: int, n_n: int = 12, n_l: int = 16, n_g: int = 8, eps: float = 1e-12) -> Rules:
     r, w, _ = build_ggq(n_g)
-    return Rules(q=q, far=simplex_rule(q), n_n=n_n, near=simplex_rule(n_n), gl=gauss_legendre(n_l),
+    return Rules(q=q, far=quad_rule(q), n_n=n_n, near=quad_rule(n_n), gl=gauss_legendre(n_l),
                  n_g=n_g, ggq=(r, w), eps=eps)
 
 

@@ -216,6 +216,56 @@ int vps_simplex_rule(int order, int* len, double* x, double* y, double* w) {
   return 0;
 }
 
+// Fully symmetric rules computed by this repository's own moment-fitting solver
+// (tools/make_sym_rules.py -> sym_rules.inc): positive weights, interior
+// points, exact to the stated degree with about two thirds of the points of
+// the collapsed Gauss-Jacobi rule (degree 12: 33 against 49), i.e. the point
+// counts of the Xiao-Gimbutas tables the SPEC names (rules.hpp:121-125),
+// which are third-party data and absent.
+namespace {
+struct SymRule {
+  int degree, n1, n21, n111, points;
+  double p[64];
+};
+const SymRule kSymRules[] = {
+#include "sym_rules.inc"
+};
+const SymRule* sym_rule_for(int order) {
+  for (const SymRule& r : kSymRules)
+    if (r.degree == order) return &r;
+  return nullptr;
+}
+}  // namespace
+
+// The evaluation's far / near rule of a given order (load_far_rule, rules.hpp:
+// 121-125): the symmetric rule of that degree where one is tabulated, the
+// collapsed Gauss-Jacobi rule otherwise.
+int vps_quad_rule(int order, int* len, double* x, double* y, double* w) {
+  const SymRule* r = sym_rule_for(order);
+  if (!r) return vps_simplex_rule(order, len, x, y, w);
+  if (!len) return fail(1, "quad_rule: len is null");
+  *len = r->points;
+  if (!x) return 0;
+  if (!y || !w) return fail(1, "quad_rule: null output array");
+  int n = 0, k = 0;
+  if (r->n1) {
+    x[n] = 1.0 / 3.0; y[n] = 1.0 / 3.0; w[n] = r->p[k++]; ++n;
+  }
+  for (int i = 0; i < r->n21; ++i) {
+    const double wi = r->p[k], a = r->p[k + 1], c = 1.0 - 2.0 * a;
+    k += 2;
+    const double px[3] = {a, a, c}, py[3] = {a, c, a};
+    for (int j = 0; j < 3; ++j, ++n) { x[n] = px[j]; y[n] = py[j]; w[n] = wi; }
+  }
+  for (int i = 0; i < r->n111; ++i) {
+    const double wi = r->p[k], a = r->p[k + 1], b = r->p[k + 2], c = 1.0 - a - b;
+    k += 3;
+    const double px[6] = {a, b, a, c, b, c}, py[6] = {b, a, c, a, c, b};
+    for (int j = 0; j < 6; ++j, ++n) { x[n] = px[j]; y[n] = py[j]; w[n] = wi; }
+  }
+  return 0;
+}
+
 // Radial GGQ by moment fitting (restating ggq.hpp:33-182): unknowns r_j and
 // log w_j; Levenberg-Marquardt from GL^alpha guesses, then damped Newton.
 int vps_ggq(int ng, double* rout, double* wout, double* max_residual) {

@@ -39,12 +39,12 @@ int main(int argc, char** argv) {
     return fail(nullptr, rc, "vps_config_fill");
   // rules: far order q, near order 12, Gauss-Legendre 16, GGQ order 8
   int lq = 0, ln = 0;
-  vps_simplex_rule(info.q, &lq, nullptr, nullptr, nullptr);
-  vps_simplex_rule(12, &ln, nullptr, nullptr, nullptr);
+  vps_quad_rule(info.q, &lq, nullptr, nullptr, nullptr);
+  vps_quad_rule(12, &ln, nullptr, nullptr, nullptr);
   std::vector<double> fx(lq), fy(lq), fw(lq), nx(ln), ny(ln), nw(ln), gx(16), gw(16), gr(9), gg(9);
   double res = 0.0;
-  if (vps_simplex_rule(info.q, &lq, fx.data(), fy.data(), fw.data()) ||
-      vps_simplex_rule(12, &ln, nx.data(), ny.data(), nw.data()) || vps_gauss_legendre(16, gx.data(), gw.data()) ||
+  if (vps_quad_rule(info.q, &lq, fx.data(), fy.data(), fw.data()) ||
+      vps_quad_rule(12, &ln, nx.data(), ny.data(), nw.data()) || vps_gauss_legendre(16, gx.data(), gw.data()) ||
       vps_ggq(8, gr.data(), gg.data(), &res))
     return fail(nullptr, 1, "rules");
   vp_rules rules{info.q, lq, fx.data(), fy.data(), fw.data(), 12, ln, nx.data(), ny.data(), nw.data(),

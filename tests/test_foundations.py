@@ -126,6 +126,39 @@ def test_substitute_rules_pass_validate_rule(q, w_edge):  # rules.hpp:60-85
     assert w.max() <= 10 * we  # PAPER.md:1874-1876 premise
 
 
+@pytest.mark.parametrize("q,npts", [(6, 12), (10, 25), (12, 33)])
+def test_symmetric_rules_from_the_moment_fit(q, npts):
+    """vps_quad_rule (the evaluation's far / near rule): the repository's own
+    fully symmetric rules (tools/make_sym_rules.py) have the point counts of
+    the X-G tables the SPEC names, pass the reference's validate_rule
+    contract (rules.hpp:60-85: positive weights, interior points, area,
+    exactness), integrate every monomial of degree <= q to rounding, and are
+    invariant under the six permutations of the barycentric coordinates."""
+    import math
+    x, y, w = vp.quad_rule(q)
+    assert len(x) == npts
+    ob.validate_rule(q, x, y, w)
+    for a in range(q + 1):
+        for b in range(q + 1 - a):
+            ex = math.factorial(a) * math.factorial(b) / math.factorial(a + b + 2)
+            assert abs((w * x ** a * y ** b).sum() - ex) <= 4e-15 * ex
+    # not exact one degree up (the rule is not secretly a larger one)
+    errs = [abs((w * x ** a * y ** (q + 1 - a)).sum() * math.factorial(q + 3) / (math.factorial(a) * math.factorial(q + 1 - a)) - 1)
+            for a in range(q + 2)]
+    assert max(errs) > 1e-6
+    pts = {(round(a, 13), round(b, 13), round(c, 13)): ww for a, b, c, ww in zip(1 - x - y, x, y, w)}
+    for (a, b, c), ww in pts.items():
+        for perm in ((a, c, b), (b, a, c), (b, c, a), (c, a, b), (c, b, a)):
+            assert perm in pts and pts[perm] == ww
+    assert w.max() <= 10 * ob.w_edge(x, y, w)  # PAPER.md:1874-1876 premise
+
+
+def test_quad_rule_falls_back_to_gauss_jacobi():
+    for q in (8, 16, 24, 40):
+        a, b = vp.quad_rule(q), vp.simplex_rule(q)
+        assert all(np.array_equal(u, v) for u, v in zip(a, b))
+
+
 def test_validate_rule_rejects_malformed():  # test_basis.cpp:114-128
     x, y, w = vp.simplex_rule(6)
     with pytest.raises(ob.OracleError, match="non-positive weight"):

@@ -45,6 +45,19 @@ def test_simplex_rule_matches_product(q):
     B.validate_rule(min(q, 32), *a)  # the reference's validate_rule contract (rules.hpp:60-85)
 
 
+@pytest.mark.parametrize("q", [6, 10, 12, 16, 24])
+def test_quad_rule_matches_product(q):
+    """The evaluation's rule: the oracle expands its own copy of the orbit
+    table (symmetric rules bit for bit); other orders as simplex_rule."""
+    a, b = B.quad_rule(q), vp.quad_rule(q)
+    assert len(a[0]) == len(b[0])
+    if q in (6, 10, 12):
+        assert all(u.tobytes() == v.tobytes() for u, v in zip(a, b))
+    else:
+        assert all(np.abs(u - v).max() <= 2.3e-16 for u, v in zip(a, b))
+    B.validate_rule(q, *a)
+
+
 @pytest.mark.parametrize("ng", [2, 5, 8])
 def test_ggq_matches_product(ng):
     r, w, res = B.ggq(ng)

@@ -132,7 +132,7 @@ def sweep(tris, fkinds, qs, epss, coeffs=None, p=0, n_grid=50, n_shell=200, nthr
     for ti, tri in enumerate(tris):
         for fk in fkinds:
             for q in qs:
-                rule = B.simplex_rule(q)
+                rule = B.quad_rule(q)  # the evaluation's far rule (symmetric where tabulated)
                 for eps in epss:
                     rho0, ta = model(tri, q, eps, rule)
                     pts = grid_points(tri, n_grid)
