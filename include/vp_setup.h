@@ -8,8 +8,10 @@
  * Reference anchors:
  *   - rules are data in the reference (rules.hpp:88-125); its
  *     Xiao-Gimbutas / Vioreanu-Rokhlin tables are absent, so
- *     vps_simplex_rule builds a collapsed Gauss-Jacobi substitute that passes
- *     the reference's validate_rule contract (rules.hpp:60-85);
+ *     vps_quad_rule gives the evaluation's far / near rules -- fully symmetric
+ *     rules from this repository's own moment-fitting solver for orders 6, 10
+ *     and 12, vps_simplex_rule's collapsed Gauss-Jacobi rule otherwise -- all
+ *     passing the reference's validate_rule contract (rules.hpp:60-85);
  *   - vps_gauss_legendre restates gauss_legendre (gauss.hpp:17-46);
  *   - vps_ggq restates build_ggq's moment fitting (ggq.hpp:33-182);
  *   - density coefficients replace the reference's callable f

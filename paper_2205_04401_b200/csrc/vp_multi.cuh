@@ -120,7 +120,7 @@ __global__ void k_shard_search(int64_t n, const int64_t* __restrict__ P, int wor
 
 // Cost model of one target (FP64 flops): the far field (direct:
 // 17 per source; FMM: the P2P of ~9 leaves of `leaf` sources plus L2P), a near
-// pair (about 6 leaves x 49 nodes x 13 flops plus a point sum) and the self
+// pair (about 6 leaves x len_n nodes x 13 flops plus a point sum) and the self
 // pair (about 16 panels x 16 nodes x 2(p+1) flops plus a point sum).
 void shard_cost_model(const vp_ctx* c, int64_t& c_far, int64_t& c_near, int64_t& c_self) {
   const int64_t S = c->n_tri * c->rules.len_q;
