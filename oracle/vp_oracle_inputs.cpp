@@ -13,6 +13,10 @@
 //                              (own algorithm: implicit-shift QL + Newton polish)
 //   simplex rule ............. collapsed Duffy map; contract of
 //                              validate_rule, rules.hpp:60-85
+//   far / near rule .......... load_far_rule, rules.hpp:121-125: fully symmetric
+//                              rules of orders 6, 10, 12 expanded from the
+//                              moment-fitted orbit table sym_rules.inc
+//                              (tools/make_sym_rules.py), else the simplex rule
 //   GGQ ...................... build_ggq, ggq.hpp:33-182 (moments :33-50,
 //                              Levenberg-Marquardt :110-139, Newton :141-164)
 //   density projection ....... L2 projection onto koornwinder_eval,
