@@ -5,16 +5,16 @@
 
 Workload (default BASELINE config 4, the largest single-GPU configuration
 and north_star's 1/2/4/8-GPU case: unit square, 1,048,576 jittered
-triangles, p = 6, q = 12, 29,360,128 staggered targets, 51,380,224 far
-sources).  One step = one full evaluation pass through the library (K3
+triangles, p = 6, q = 12, 29,360,128 staggered targets, 34,603,008 far
+sources: 33 per triangle, the symmetric order-12 rule).  One step = one full evaluation pass through the library (K3
 near-field lists, K1 strengths, K2 direct far sum, K4 near pairs, K5 self
 pairs, assembly) over one batch of targets:
 
   * headline `value` -- the direct far path (north_star part 3) over a
     deterministic target subset: the config's targets in Morton order, every
-    `stride`-th (config 4: every 256th, 114,688 targets), each with its full
-    51.4 M-source far field (SURVEY.md §7/§8(d) allow a stated fixed subset;
-    a full direct config-4 step is about 20 minutes).  Strong scaling: the
+    `stride`-th (config 4: every 128th, 229,376 targets), each with its full
+    34.6 M-source far field (SURVEY.md §7/§8(d) allow a stated fixed subset;
+    a full direct config-4 step is about 13 minutes).  Strong scaling: the
     job is that subset whatever N, cut into N contiguous Morton shards.
   * `pair_stage` -- the near/self corrections of ALL the config's targets
     (far method "none"): BASELINE's second metric, near-field pair
