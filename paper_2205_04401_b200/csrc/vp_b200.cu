@@ -319,7 +319,7 @@ __global__ void k_pair_tgt(int64_t T, const int64_t* __restrict__ off, int32_t* 
 #define VP_NEAR_MINB 2
 #endif
 #ifndef VP_SELF_MINB
-#define VP_SELF_MINB 6
+#define VP_SELF_MINB 5
 #endif
 #ifndef VP_FAR_MINB
 #define VP_FAR_MINB 2
