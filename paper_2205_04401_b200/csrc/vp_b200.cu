@@ -1662,8 +1662,20 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
 // for K8 nodes, against 4 per node in k_near_cg) and the G values of its K8
 // nodes (8 consecutive doubles per leaf and slot) a group ahead.  Same zero
 // rows past a batch and the same fixed summation order per target.
-template <int K8>
-__global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
+// W warps per block, two blocks per SM.  The register budget follows from W
+// (65536 / (2 * 32 W)): the 7 slots of a 49-node rule need 126 registers
+// (W = 8), the 5 slots of the 33-node rule fit 96 without spills and run
+// faster at W = 10 (20 warps per SM: 43.5 against 46.6 ms on config 4; 9, 11
+// and 12 warps: 49.3, 47.2, 46.5 ms).
+template <int W>
+struct LeafRowsW {
+  double2 d0[W][kLeafRows];
+  double2 ba[W][kLeafRows];
+  double2 ca[W][kLeafRows];
+  ulonglong2 g[W][kLeafRows];  // .x: address of the leaf's cache row
+};
+template <int K8, int W>
+__global__ void __launch_bounds__(W * 32, 2)
     k_near_c8(int64_t T, const int64_t* __restrict__ tl, const int32_t* __restrict__ pair_elem,
               const double2* __restrict__ txy, const ElemRec* __restrict__ el, const int64_t* __restrict__ loff,
               const unsigned long long* __restrict__ leaves, const RulesDev* __restrict__ R,
@@ -1671,10 +1683,10 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
               const double* __restrict__ slot_ref, int cache_depth, double* __restrict__ part_t, unsigned c3ff) {
   extern __shared__ __align__(16) unsigned char nsm[];
   double2* tab = reinterpret_cast<double2*>(nsm);  // kLogEntries x kLogCopies
-  __shared__ LeafRows sR;
+  __shared__ LeafRowsW<W> sR;
   const int nslot = cache_depth >= 0 ? ((1 << (2 * (cache_depth + 1))) - 1) / 3 : 0;
   for (int i = threadIdx.x; i < kLogEntries * kLogCopies; i += blockDim.x) tab[i] = g_logtab[i / kLogCopies];
-  for (int i = threadIdx.x; i < NG_WARPS * kLeafRows; i += blockDim.x) {
+  for (int i = threadIdx.x; i < W * kLeafRows; i += blockDim.x) {
     (&sR.d0[0][0])[i] = (&sR.ba[0][0])[i] = (&sR.ca[0][0])[i] = make_double2(0.0, 0.0);
     (&sR.g[0][0])[i] = make_ulonglong2((unsigned long long)zrow, 0ull);
   }
@@ -1695,7 +1707,7 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
   // Targets in grid-stride order; target t's cached leaves are
   // [tl[t], tl[t + 1]) (tl[t] = loff[toff[t]], one load deep), and the codes
   // of the next batch are loaded while the current batch computes.
-  for (int64_t t = (int64_t)blockIdx.x * NG_WARPS + wid; t < T; t += (int64_t)gridDim.x * NG_WARPS) {
+  for (int64_t t = (int64_t)blockIdx.x * W + wid; t < T; t += (int64_t)gridDim.x * W) {
     const int64_t L0 = tl[t], L1 = tl[t + 1];
     double acc = 0.0, acc1 = 0.0;
     if (L1 > L0) {
@@ -3219,10 +3231,11 @@ inline int near_group_shape(int Ln, int* S_out) {
 template <int K8>
 void launch_near_c8(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
                     const double* gc) {
-  const int blocks = (int)std::min<int64_t>(nblk(T, NG_WARPS), (int64_t)c->sm_count * 24);
+  constexpr int W = K8 <= 5 ? 10 : 8;  // warps per block (see k_near_c8)
+  const int blocks = (int)std::min<int64_t>(nblk(T, W), (int64_t)c->sm_count * 24);
   k_tgt_leafrange<<<nblk(T + 1, 256), 256, 0, c->stream>>>(T, toff, c->d_loffc.as<int64_t>(), c->d_tl.as<int64_t>());
   c->last_launches += 1;
-  k_near_c8<K8><<<std::max(blocks, 1), NG_WARPS * 32, sizeof(LogTab), c->stream>>>(
+  k_near_c8<K8, W><<<std::max(blocks, 1), W * 32, sizeof(LogTab), c->stream>>>(
       T, c->d_tl.as<int64_t>(), pelem, txy, c->d_el.as<ElemRec>(), c->d_loffc.as<int64_t>(), c->d_leafc.as<unsigned long long>(),
       c->d_rules.as<RulesDev>(), gc, gc + c->n_tri * (int64_t)(((1ll << (2 * (c->cache_depth + 1))) - 1) / 3) *
       c->rules.len_n, c->d_slotref.as<double>(), c->cache_depth, c->d_neart.as<double>(), 0x3ff00000u);
@@ -4382,14 +4395,14 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_self<10, self_gs(10)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<11, self_gs(11)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<12, self_gs(12)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<1, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<3, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<4, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<5, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<7, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
