@@ -1664,9 +1664,11 @@ __global__ void __launch_bounds__(NG_WARPS * 32, VP_NG_MINB)
 // rows past a batch and the same fixed summation order per target.
 // W warps per block, two blocks per SM.  The register budget follows from W
 // (65536 / (2 * 32 W)): the 7 slots of a 49-node rule need 126 registers
-// (W = 8), the 5 slots of the 33-node rule fit 96 without spills and run
-// faster at W = 10 (20 warps per SM: 43.5 against 46.6 ms on config 4; 9, 11
-// and 12 warps: 49.3, 47.2, 46.5 ms).
+// (W = 8).  The 5 slots of the 33-node rule fit 96 without spills and the
+// kernel alone runs faster at W = 10 (20 warps per SM: 43.5 against 46.6 ms
+// on config 4; 9, 11 and 12 warps: 49.3, 47.2, 46.5 ms), but beside the FMM
+// stream the evaluation is slower with it (250 against 211 ms per step: the
+// pair stage stretches to 211 ms), so W stays 8.
 template <int W>
 struct LeafRowsW {
   double2 d0[W][kLeafRows];
@@ -3231,7 +3233,7 @@ inline int near_group_shape(int Ln, int* S_out) {
 template <int K8>
 void launch_near_c8(vp_ctx* c, int64_t T, const int64_t* toff, const int32_t* pelem, const double2* txy,
                     const double* gc) {
-  constexpr int W = K8 <= 5 ? 10 : 8;  // warps per block (see k_near_c8)
+  constexpr int W = 8;  // warps per block (see k_near_c8: 10 is faster alone, slower beside the FMM)
   const int blocks = (int)std::min<int64_t>(nblk(T, W), (int64_t)c->sm_count * 24);
   k_tgt_leafrange<<<nblk(T + 1, 256), 256, 0, c->stream>>>(T, toff, c->d_loffc.as<int64_t>(), c->d_tl.as<int64_t>());
   c->last_launches += 1;
@@ -4395,11 +4397,11 @@ int vp_create(int device, vp_ctx** out) {
       cudaFuncSetAttribute(k_self<10, self_gs(10)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(10)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<11, self_gs(11)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(11)) != cudaSuccess ||
       cudaFuncSetAttribute(k_self<12, self_gs(12)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)self_dyn_smem(12)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<1, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<3, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<4, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
-      cudaFuncSetAttribute(k_near_c8<5, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
+      cudaFuncSetAttribute(k_near_c8<5, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<7, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
       cudaFuncSetAttribute(k_near_c8<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LogTab)) != cudaSuccess ||
